@@ -1,0 +1,154 @@
+"""ctypes binding of the sm_100a C ABI (include/cbrng_b200.h).
+
+The product path has exactly one implementation: the CUDA kernels in
+`_lib/libcbrng_b200.so`. There is no CPU fallback — if the library or a CUDA
+device is missing, every generating call raises RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+import threading
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_DIR = PKG / "_lib"
+LIB_PATH = LIB_DIR / "libcbrng_b200.so"
+CURAND_LIB_PATH = LIB_DIR / "libcbrng_curand_baseline.so"
+HEADER = PKG.parent / "include" / "cbrng_b200.h"
+
+CBRNG_OK, CBRNG_EINVAL, CBRNG_EALG, CBRNG_ECUDA, CBRNG_EALIGN = 0, -1, -2, -3, -4
+BROWNIAN_PER_STEP, BROWNIAN_FUSED = 0, 1
+
+_lock = threading.Lock()
+_lib = None
+_curand = None
+
+u8p = C.POINTER(C.c_uint8)
+vp = C.c_void_p
+u32, u64, i32, f64 = C.c_uint32, C.c_uint64, C.c_int, C.c_double
+
+# name -> (restype, argtypes); mirrors include/cbrng_b200.h
+SIGNATURES = {
+    "cbrng_version": (C.c_char_p, []),
+    "cbrng_last_error": (C.c_char_p, []),
+    "cbrng_device_sm_count": (i32, [i32]),
+    "cbrng_words": (i32, [i32, u64, u32, u32, vp, u64, vp, vp, vp]),
+    "cbrng_uniform_f32": (i32, [i32, u64, u32, u32, vp, u64, vp, vp, vp]),
+    "cbrng_uniform_f64": (i32, [i32, u64, u32, u32, vp, u64, vp, vp, vp]),
+    "cbrng_normal2_f64": (i32, [i32, u64, u32, u32, vp, u64, vp, vp, vp, vp]),
+    "cbrng_tyche_fill": (i32, [vp, u64, vp, vp]),
+    "cbrng_prefix_words": (i32, [i32, vp, u64, vp, u32, u64, u32, vp, vp]),
+    "cbrng_prefix_uniform_f32": (i32, [i32, vp, u64, vp, u32, u64, u32, vp, vp]),
+    "cbrng_philox_block_lanes": (i32, [vp, vp, u64, u64, vp, vp]),
+    "cbrng_philox4x32": (i32, [vp, vp, u64, vp, vp]),
+    "cbrng_threefry4x32": (i32, [vp, vp, i32, u64, vp, vp]),
+    "cbrng_squares32": (i32, [vp, vp, u64, vp, vp]),
+    "cbrng_squares_keys": (i32, [vp, u64, vp, vp]),
+    "cbrng_tyche_mix": (i32, [vp, u64, u32, vp]),
+    "cbrng_tyche_init": (i32, [vp, u64, vp, u32, u64, vp, vp]),
+    "cbrng_brownian_init": (i32, [i32, u64, vp, u64, u32, vp, vp, vp, vp, vp]),
+    "cbrng_brownian_steps": (i32, [i32, u64, vp, u64, vp, vp, vp, vp, u32, u64, u64, f64, f64, f64, i32, vp]),
+    "cbrng_brownian_stats": (i32, [u64, vp, u64, vp, vp, vp, vp, vp, vp]),
+    "cbrng_digest_u32": (i32, [vp, u64, u64, vp, vp]),
+    "cbrng_fnv1a64": (u64, [vp, u64, u64]),
+}
+
+CURAND_SIGNATURES = {
+    "cbrng_curand_last_error": (C.c_char_p, []),
+    "cbrng_curand_create": (vp, [u64, vp]),
+    "cbrng_curand_destroy": (i32, [vp]),
+    "cbrng_curand_set_offset": (i32, [vp, u64]),
+    "cbrng_curand_u32": (i32, [vp, vp, u64]),
+    "cbrng_curand_uniform_f32": (i32, [vp, vp, u64]),
+    "cbrng_curand_uniform_f64": (i32, [vp, vp, u64]),
+    "cbrng_curand_normal_f64": (i32, [vp, vp, u64]),
+    "cbrng_curand_state_bytes": (u64, []),
+    "cbrng_curand_brownian_init": (i32, [vp, u64, vp, vp, vp, vp, vp]),
+    "cbrng_curand_brownian_steps": (i32, [vp, u64, vp, vp, vp, vp, u64, f64, f64, f64, i32, vp]),
+}
+
+
+def build(force: bool = False) -> None:
+    """Compile the CUDA libraries in-tree (make -C csrc); nvcc cross-compiles without a GPU."""
+    cmd = ["make", "-s", "-j8", "-C", str(PKG / "csrc")]
+    if force:
+        subprocess.run(["make", "-s", "-C", str(PKG / "csrc"), "clean"], check=True)
+    subprocess.run(cmd, check=True)
+
+
+def _bind(path: Path, sigs: dict):
+    L = C.CDLL(str(path))
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+def lib():
+    """The product library. Raises RuntimeError if it was not built."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not LIB_PATH.exists():
+                    raise RuntimeError(
+                        f"CUDA library {LIB_PATH} is missing; run paper_2310_19925_b200._lib.build() "
+                        "(there is no CPU fallback)")
+                _lib = _bind(LIB_PATH, SIGNATURES)
+    return _lib
+
+
+def curand_lib():
+    global _curand
+    if _curand is None:
+        with _lock:
+            if _curand is None:
+                _curand = _bind(CURAND_LIB_PATH, CURAND_SIGNATURES)
+    return _curand
+
+
+def last_error() -> str:
+    msg = lib().cbrng_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map C-ABI status codes onto the reference's exception types."""
+    if rc == CBRNG_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc in (CBRNG_EINVAL, CBRNG_EALG):
+        raise ValueError(msg)
+    raise RuntimeError(msg)
+
+
+def require_cuda():
+    """Fail loudly when no CUDA device is present (no CPU fallback)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2310_19925_b200 needs a CUDA device (B200); no CPU fallback exists")
+    lib()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def header_symbols() -> list[str]:
+    """Function names declared in include/cbrng_b200.h."""
+    import re
+
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(cbrng_[a-z0-9_]+)\s*\(", text, re.M)))

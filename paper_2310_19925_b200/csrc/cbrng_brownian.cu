@@ -1,0 +1,291 @@
+// cbrng_brownian.cu — the paper's Brownian-dynamics benchmark (PAPER.md:100-139,
+// :263) with the reference semantics of brownian.py:107-195.
+//
+// Particles are SoA float64 (x, y, vx, vy) in HBM; pid is implicit (pid_base + i)
+// or an explicit u64 array. Randomness is re-derived every step from the stream
+// (seed = pid, counter = init_counter + it): no RNG state exists anywhere, and
+// no random buffer is materialised — the 4 words are produced in registers
+// and consumed by the update in the same thread.
+//
+// Two step kernels share one device function:
+//   * PER_STEP: one launch per step, 64 B of HBM traffic per particle-step
+//     (the paper's kernel shape; HBM-bound);
+//   * FUSED: the particle stays in registers for all steps (particles are
+//     independent, brownian.py:158-161, so this is a legal reordering); the
+//     pid-only part of the key schedule is hoisted out of the step loop.
+//     INT/FP64-pipe-bound.
+//
+// FP64 arithmetic is bit-exact with numpy's evaluation order:
+//   vx -= ((gamma/mass) * vx) * dt;  vx += (r * 2.0 - 1.0) * sqrt(dt);  x += vx * dt
+// with every operation an explicit round-to-nearest intrinsic (no FMA contraction).
+#include "cbrng_internal.cuh"
+
+namespace cbrng {
+
+struct BrownArgs {
+    uint64_t n;
+    const uint64_t *pid;
+    uint64_t pid_base;
+    double *x, *y, *vx, *vy;
+    uint32_t init_ctr;
+    uint64_t first_it;
+    uint64_t nsteps;
+    double gm, dt, sqrt_dt;
+};
+
+// Per-particle, step-invariant state.
+template <int ALG> struct Particle;
+template <> struct Particle<PHILOX> {
+    PhiloxParticle p;
+    __device__ __forceinline__ explicit Particle(uint64_t pid) : p(philox_particle_setup(pid)) {}
+    __device__ __forceinline__ uint4 words(uint32_t ctr) const {
+        uint32_t mh, ml;
+        mulhilo(PHILOX_M0, ctr, mh, ml);
+        return philox_particle_block(p, mh, ml);
+    }
+};
+template <> struct Particle<THREEFRY> {
+    uint32_t k0, k1;
+    __device__ __forceinline__ explicit Particle(uint64_t pid) : k0((uint32_t)pid), k1((uint32_t)(pid >> 32)) {}
+    __device__ __forceinline__ uint4 words(uint32_t ctr) const {
+        return threefry_block(make_uint4(0, 0, 0, 0), k0, k1, ctr, 0);
+    }
+};
+template <> struct Particle<SQUARES> {
+    uint64_t key;
+    __device__ __forceinline__ explicit Particle(uint64_t pid) : key(squares_key(pid)) {}
+    __device__ __forceinline__ uint32_t w(uint64_t x) const {
+        uint64_t y = x, z = y + key;
+        x = swap32(x * x + y);
+        x = swap32(x * x + z);
+        x = swap32(x * x + y);
+        return (uint32_t)((x * x + z) >> 32);
+    }
+    __device__ __forceinline__ uint4 words(uint32_t ctr) const {
+        uint64_t x0 = ((uint64_t)ctr << 32) * key;  // counter (ctr << 32) | k, k = 0..3
+        return make_uint4(w(x0), w(x0 + key), w(x0 + 2 * key), w(x0 + 3 * key));
+    }
+};
+template <> struct Particle<TYCHE> {
+    uint64_t pid;
+    __device__ __forceinline__ explicit Particle(uint64_t p) : pid(p) {}
+    __device__ __forceinline__ uint4 words(uint32_t ctr) const {
+        uint4 s = tyche_init(pid, ctr);
+        uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
+        uint4 w;
+        tyche_mix(a, b, c, d); w.x = b;
+        tyche_mix(a, b, c, d); w.y = b;
+        tyche_mix(a, b, c, d); w.z = b;
+        tyche_mix(a, b, c, d); w.w = b;
+        return w;
+    }
+};
+
+// Words 0..7 of stream (pid, ctr) for init_particles.
+template <int ALG>
+__device__ __forceinline__ void words8(uint64_t pid, uint32_t ctr, uint4 &w0, uint4 &w1) {
+    if constexpr (ALG == PHILOX) {
+        w0 = philox_block(make_uint4(ctr, 0, 0, 0), (uint32_t)pid, (uint32_t)(pid >> 32));
+        w1 = philox_block(make_uint4(ctr, 1, 0, 0), (uint32_t)pid, (uint32_t)(pid >> 32));
+    } else if constexpr (ALG == THREEFRY) {
+        w0 = threefry_block(make_uint4(0, 0, 0, 0), (uint32_t)pid, (uint32_t)(pid >> 32), ctr, 0);
+        w1 = threefry_block(make_uint4(1, 0, 0, 0), (uint32_t)pid, (uint32_t)(pid >> 32), ctr, 0);
+    } else if constexpr (ALG == SQUARES) {
+        uint64_t key = squares_key(pid), base = ((uint64_t)ctr << 32);
+        w0 = make_uint4(squares_round(key, base | 0), squares_round(key, base | 1), squares_round(key, base | 2),
+                        squares_round(key, base | 3));
+        w1 = make_uint4(squares_round(key, base | 4), squares_round(key, base | 5), squares_round(key, base | 6),
+                        squares_round(key, base | 7));
+    } else {
+        uint4 s = tyche_init(pid, ctr);
+        uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
+        tyche_mix(a, b, c, d); w0.x = b;
+        tyche_mix(a, b, c, d); w0.y = b;
+        tyche_mix(a, b, c, d); w0.z = b;
+        tyche_mix(a, b, c, d); w0.w = b;
+        tyche_mix(a, b, c, d); w1.x = b;
+        tyche_mix(a, b, c, d); w1.y = b;
+        tyche_mix(a, b, c, d); w1.z = b;
+        tyche_mix(a, b, c, d); w1.w = b;
+    }
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(256) brownian_init_kernel(const __grid_constant__ BrownArgs a) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t pid = a.pid ? a.pid[i] : a.pid_base + i;
+        uint4 w0, w1;
+        words8<ALG>(pid, a.init_ctr, w0, w1);
+        a.x[i] = u32x2_to_f64(w0.x, w0.y);
+        a.y[i] = u32x2_to_f64(w0.z, w0.w);
+        a.vx[i] = __dsub_rn(__dmul_rn(u32x2_to_f64(w1.x, w1.y), 2.0), 1.0);
+        a.vy[i] = __dsub_rn(__dmul_rn(u32x2_to_f64(w1.z, w1.w), 2.0), 1.0);
+    }
+}
+
+// One dynamics step of one particle (brownian.py:129-142).
+__device__ __forceinline__ void step_update(double &x, double &y, double &vx, double &vy, uint4 w, double gm, double dt,
+                                            double sqrt_dt) {
+    vx = __dsub_rn(vx, __dmul_rn(__dmul_rn(gm, vx), dt));
+    vy = __dsub_rn(vy, __dmul_rn(__dmul_rn(gm, vy), dt));
+    const double rx = u32x2_to_f64(w.x, w.y);
+    const double ry = u32x2_to_f64(w.z, w.w);
+    vx = __dadd_rn(vx, __dmul_rn(__dsub_rn(__dmul_rn(rx, 2.0), 1.0), sqrt_dt));
+    vy = __dadd_rn(vy, __dmul_rn(__dsub_rn(__dmul_rn(ry, 2.0), 1.0), sqrt_dt));
+    x = __dadd_rn(x, __dmul_rn(vx, dt));
+    y = __dadd_rn(y, __dmul_rn(vy, dt));
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(256) brownian_steps_kernel(const __grid_constant__ BrownArgs a) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t pid = a.pid ? a.pid[i] : a.pid_base + i;
+        double x = a.x[i], y = a.y[i], vx = a.vx[i], vy = a.vy[i];
+        const Particle<ALG> P(pid);
+        uint32_t ctr = a.init_ctr + (uint32_t)a.first_it;
+        for (uint64_t s = 0; s < a.nsteps; s++, ctr++) {
+            step_update(x, y, vx, vy, P.words(ctr), a.gm, a.dt, a.sqrt_dt);
+        }
+        a.x[i] = x; a.y[i] = y; a.vx[i] = vx; a.vy[i] = vy;
+    }
+}
+
+// ---------------- deterministic statistics ----------------
+__device__ __forceinline__ int64_t fixq(double v, double scale) { return __double2ll_rn(v * scale); }
+
+__global__ void __launch_bounds__(256) brownian_stats_kernel(uint64_t n, const uint64_t *pid, uint64_t pid_base,
+                                                             const double *x, const double *y, const double *vx,
+                                                             const double *vy, int64_t *acc) {
+    int64_t s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t p = pid ? pid[i] : pid_base + i;
+        const double X = x[i], Y = y[i], VX = vx[i], VY = vy[i];
+        s[0] += 1;
+        s[1] += fixq(X, 0x1p32);
+        s[2] += fixq(Y, 0x1p32);
+        s[3] += fixq(VX, 0x1p32);
+        s[4] += fixq(VY, 0x1p32);
+        s[5] += fixq(__dadd_rn(__dmul_rn(X, X), __dmul_rn(Y, Y)), 0x1p24);
+        s[6] += fixq(__dadd_rn(__dmul_rn(VX, VX), __dmul_rn(VY, VY)), 0x1p24);
+        uint64_t h = mix64(p ^ 0x5851F42D4C957F2Dull);
+        h = mix64(h ^ (uint64_t)__double_as_longlong(X));
+        h = mix64(h ^ (uint64_t)__double_as_longlong(Y));
+        h = mix64(h ^ (uint64_t)__double_as_longlong(VX));
+        h = mix64(h ^ (uint64_t)__double_as_longlong(VY));
+        s[7] += (int64_t)h;
+    }
+    __shared__ int64_t red[8][8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        int64_t v = s[k];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[w][k] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        int64_t v = 0;
+        for (int j = 0; j < (int)(blockDim.x >> 5); j++) v += red[j][threadIdx.x];
+        atomicAdd(reinterpret_cast<unsigned long long *>(acc) + threadIdx.x, (unsigned long long)v);
+    }
+}
+
+__global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint64_t n, uint64_t off, uint64_t *acc) {
+    uint64_t s = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        s += mix64(mix64(off + i) ^ (uint64_t)w[i]);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __shared__ uint64_t red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t v = 0;
+        for (int j = 0; j < (int)(blockDim.x >> 5); j++) v += red[j];
+        atomicAdd(reinterpret_cast<unsigned long long *>(acc), (unsigned long long)v);
+    }
+}
+
+template <int ALG>
+static int launch_steps(BrownArgs a, int mode, cudaStream_t st) {
+    auto k = brownian_steps_kernel<ALG>;
+    // One thread per particle: the fused kernel needs every particle resident
+    // or queued, so the grid covers n (no persistence).
+    const unsigned grid = (unsigned)((a.n + 255) / 256);
+    if (mode == CBRNG_BROWNIAN_FUSED) {
+        k<<<grid, 256, 0, st>>>(a);
+        return check_launch("brownian_steps_kernel");
+    }
+    const uint64_t total = a.nsteps;
+    a.nsteps = 1;
+    for (uint64_t s = 0; s < total; s++) {
+        k<<<grid, 256, 0, st>>>(a);
+        a.first_it += 1;
+    }
+    return check_launch("brownian_steps_kernel");
+}
+
+}  // namespace cbrng
+
+using namespace cbrng;
+
+extern "C" {
+
+int cbrng_brownian_init(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_base, uint32_t init_ctr, double *x,
+                        double *y, double *vx, double *vy, void *stream) {
+    CBRNG_CHECK_ALG(alg);
+    clear_error();
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(x && y && vx && vy, "NULL particle array");
+    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, 0, 0, 0.0, 0.0, 0.0};
+    cudaStream_t st = as_stream(stream);
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    switch (alg) {
+        case PHILOX: brownian_init_kernel<PHILOX><<<grid, 256, 0, st>>>(a); break;
+        case THREEFRY: brownian_init_kernel<THREEFRY><<<grid, 256, 0, st>>>(a); break;
+        case SQUARES: brownian_init_kernel<SQUARES><<<grid, 256, 0, st>>>(a); break;
+        default: brownian_init_kernel<TYCHE><<<grid, 256, 0, st>>>(a); break;
+    }
+    return check_launch("brownian_init_kernel");
+}
+
+int cbrng_brownian_steps(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_base, double *x, double *y, double *vx,
+                         double *vy, uint32_t init_ctr, uint64_t first_it, uint64_t nsteps, double gamma, double mass,
+                         double dt, int mode, void *stream) {
+    CBRNG_CHECK_ALG(alg);
+    clear_error();
+    CBRNG_REQUIRE(first_it >= 1, "iteration must be >= 1; counter 0 is reserved for init");
+    CBRNG_REQUIRE(mode == CBRNG_BROWNIAN_PER_STEP || mode == CBRNG_BROWNIAN_FUSED, "bad mode %d", mode);
+    CBRNG_REQUIRE(mass > 0.0 && gamma >= 0.0 && dt >= 0.0, "bad physical parameters");
+    if (n == 0 || nsteps == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(x && y && vx && vy, "NULL particle array");
+    // Host-side scalars exactly as the reference forms them (brownian.py:134, :177).
+    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, first_it, nsteps, gamma / mass, dt, std::sqrt(dt)};
+    cudaStream_t st = as_stream(stream);
+    switch (alg) {
+        case PHILOX: return launch_steps<PHILOX>(a, mode, st);
+        case THREEFRY: return launch_steps<THREEFRY>(a, mode, st);
+        case SQUARES: return launch_steps<SQUARES>(a, mode, st);
+        default: return launch_steps<TYCHE>(a, mode, st);
+    }
+}
+
+int cbrng_brownian_stats(uint64_t n, const uint64_t *pid, uint64_t pid_base, const double *x, const double *y,
+                         const double *vx, const double *vy, int64_t *acc, void *stream) {
+    clear_error();
+    CBRNG_REQUIRE(acc, "acc is NULL");
+    if (n == 0) return CBRNG_OK;
+    auto k = brownian_stats_kernel;
+    k<<<grid_for(k, 256, 0, (n + 255) / 256), 256, 0, as_stream(stream)>>>(n, pid, pid_base, x, y, vx, vy, acc);
+    return check_launch("brownian_stats_kernel");
+}
+
+int cbrng_digest_u32(const uint32_t *words, uint64_t n, uint64_t global_offset, uint64_t *acc, void *stream) {
+    clear_error();
+    CBRNG_REQUIRE(acc, "acc is NULL");
+    if (n == 0) return CBRNG_OK;
+    auto k = digest_u32_kernel;
+    k<<<grid_for(k, 256, 0, (n + 255) / 256), 256, 0, as_stream(stream)>>>(words, n, global_offset, acc);
+    return check_launch("digest_u32_kernel");
+}
+
+}  // extern "C"

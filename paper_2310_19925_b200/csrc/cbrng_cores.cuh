@@ -1,0 +1,389 @@
+// cbrng_cores.cuh — register-resident counter-based generator cores for sm_100a.
+//
+// Bit-exact restatements of the reference algorithms
+// (/root/reference/pkg/src/cbrng/generators.py:97-224), written for the GPU:
+// every function is a pure function of (key, counter) kept in registers, with
+// no global state. Launch-uniform work (round-key schedules, the parts of the
+// first rounds that depend only on (seed, stream counter)) is folded on the
+// host into kernel parameters, so it costs zero per-element instructions: the
+// LOP3s read it straight from the constant bank.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cbrng {
+
+enum Alg : int { PHILOX = 0, THREEFRY = 1, SQUARES = 2, TYCHE = 3 };
+
+// generators.py:35-54
+constexpr uint32_t PHILOX_M0 = 0xD2511F53u;
+constexpr uint32_t PHILOX_M1 = 0xCD9E8D57u;
+constexpr uint32_t PHILOX_W0 = 0x9E3779B9u;
+constexpr uint32_t PHILOX_W1 = 0xBB67AE85u;
+constexpr uint32_t THREEFRY_PARITY = 0x1BD11BDAu;
+constexpr uint32_t TYCHE_INIT_CONST = 0x9E3779B9u;
+constexpr uint64_t GOLDEN64 = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t SPLITMIX_M1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t SPLITMIX_M2 = 0x94D049BB133111EBull;
+
+__host__ __device__ __forceinline__ uint32_t rotl32(uint32_t x, int r) {
+#ifdef __CUDA_ARCH__
+    return __funnelshift_l(x, x, r);  // SHF.L.W
+#else
+    return (x << r) | (x >> (32 - r));
+#endif
+}
+
+__host__ __device__ __forceinline__ void mulhilo(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
+    uint64_t p = (uint64_t)a * b;  // IMAD.WIDE.U32
+    hi = (uint32_t)(p >> 32);
+    lo = (uint32_t)p;
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (generators.py:101-122)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
+                                                      uint32_t k0, uint32_t k1) {
+    uint32_t h0, l0, h1, l1;
+    mulhilo(PHILOX_M0, c0, h0, l0);
+    mulhilo(PHILOX_M1, c2, h1, l1);
+    c0 = h1 ^ c1 ^ k0;
+    c1 = l1;
+    c2 = h0 ^ c3 ^ k1;
+    c3 = l0;
+}
+
+// Generic block: per-element key schedule (used where the key varies per lane).
+__host__ __device__ __forceinline__ uint4 philox_block(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        philox_round(c.x, c.y, c.z, c.w, k0, k1);
+        k0 += PHILOX_W0;
+        k1 += PHILOX_W1;
+    }
+    return c;
+}
+
+// Single stream (key, stream counter sc) with ctr = (sc, bc, 0, 0): rounds 0-3
+// partially depend only on (key, sc). The host folds those parts into this
+// struct (philox_stream_setup) and the device runs 16 IMAD.WIDE + 18 LOP per
+// block instead of 20 + 20 (+18 key adds).
+struct PhiloxStream {
+    uint32_t k0_0;    // round 0: c0 = bc ^ k0_0
+    uint32_t a1;      // round 1: c2 = hi(M0*c0) ^ a1
+    uint32_t b2, c2;  // round 2: c0 = hi(M1*c2) ^ b2 ; c2 = c3 ^ c2k
+    uint32_t v0, v1;  // round-1 uniform outputs (c0, c1)
+    uint32_t k0_3, e3;  // round 3: c0 = hi(M1*c2) ^ c1 ^ k0_3 ; c2 = hi(M0*c0) ^ e3
+    uint32_t rk0[6], rk1[6];  // rounds 4..9
+};
+
+inline PhiloxStream philox_stream_setup(uint64_t seed, uint32_t sc) {
+    uint32_t K0[10], K1[10];
+    K0[0] = (uint32_t)seed;
+    K1[0] = (uint32_t)(seed >> 32);
+    for (int r = 1; r < 10; r++) { K0[r] = K0[r - 1] + PHILOX_W0; K1[r] = K1[r - 1] + PHILOX_W1; }
+    PhiloxStream p;
+    uint32_t h, l;
+    // round 0 with c = (sc, bc, 0, 0): p0 = M0*sc, p1 = 0
+    mulhilo(PHILOX_M0, sc, h, l);
+    uint32_t u2 = h ^ K1[0], u3 = l;  // c2, c3 after round 0; c0 = bc ^ K0[0], c1 = 0
+    p.k0_0 = K0[0];
+    // round 1: p0 = M0*c0 (varies), p1 = M1*u2 (uniform)
+    mulhilo(PHILOX_M1, u2, h, l);
+    p.v0 = h ^ 0u ^ K0[1];
+    p.v1 = l;
+    p.a1 = u3 ^ K1[1];  // c2 = hi(M0*c0) ^ c3(=u3) ^ K1[1]; c3 = lo(M0*c0)
+    // round 2: p0 = M0*v0 (uniform), p1 = M1*c2 (varies)
+    mulhilo(PHILOX_M0, p.v0, h, l);
+    p.b2 = p.v1 ^ K0[2];  // c0 = hi(M1*c2) ^ v1 ^ K0[2]; c1 = lo(M1*c2)
+    p.c2 = h ^ K1[2];     // c2 = hi(M0*v0) ^ c3 ^ K1[2]
+    uint32_t d = l;       // c3 = lo(M0*v0)
+    // round 3: c2 = hi(M0*c0) ^ d ^ K1[3]
+    p.k0_3 = K0[3];
+    p.e3 = d ^ K1[3];
+    for (int r = 4; r < 10; r++) { p.rk0[r - 4] = K0[r]; p.rk1[r - 4] = K1[r]; }
+    return p;
+}
+
+__device__ __forceinline__ uint4 philox_stream_block(const PhiloxStream& p, uint32_t bc) {
+    uint32_t c0, c1, c2, c3, h, l;
+    // round 0
+    c0 = bc ^ p.k0_0;
+    // round 1
+    mulhilo(PHILOX_M0, c0, h, l);
+    c2 = h ^ p.a1;
+    c3 = l;
+    // round 2
+    mulhilo(PHILOX_M1, c2, h, l);
+    c0 = h ^ p.b2;
+    c1 = l;
+    c2 = c3 ^ p.c2;
+    // round 3 (c3 of round 2 is uniform and folded into e3)
+    {
+        uint32_t h0, l0, h1, l1;
+        mulhilo(PHILOX_M0, c0, h0, l0);
+        mulhilo(PHILOX_M1, c2, h1, l1);
+        c0 = h1 ^ c1 ^ p.k0_3;
+        c1 = l1;
+        c2 = h0 ^ p.e3;
+        c3 = l0;
+    }
+#pragma unroll
+    for (int r = 0; r < 6; r++) philox_round(c0, c1, c2, c3, p.rk0[r], p.rk1[r]);
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// Per-particle Philox for the Brownian walk: key = pid, ctr = (counter, 0, 0, 0).
+// Everything that depends only on pid is hoisted out of the step loop.
+struct PhiloxParticle {
+    uint32_t k0[10], k1[10];
+    uint32_t q1;       // round 1: c2 = c3 ^ q1, q1 = hi(M0*pid_lo) ^ K1[1]
+    uint32_t p0lo;     // round 1: c3 = lo(M0*pid_lo)
+    uint32_t r2;       // round 2: c2 = hi(M0*c0) ^ r2, r2 = p0lo ^ K1[2]
+};
+
+__device__ __forceinline__ PhiloxParticle philox_particle_setup(uint64_t pid) {
+    PhiloxParticle p;
+    p.k0[0] = (uint32_t)pid;
+    p.k1[0] = (uint32_t)(pid >> 32);
+#pragma unroll
+    for (int r = 1; r < 10; r++) { p.k0[r] = p.k0[r - 1] + PHILOX_W0; p.k1[r] = p.k1[r - 1] + PHILOX_W1; }
+    uint32_t h, l;
+    mulhilo(PHILOX_M0, p.k0[0], h, l);
+    p.q1 = h ^ p.k1[1];
+    p.p0lo = l;
+    p.r2 = l ^ p.k1[2];
+    return p;
+}
+
+// Block 0 of stream (pid, ctr); mh/ml = hi/lo(M0*ctr) are step-uniform.
+__device__ __forceinline__ uint4 philox_particle_block(const PhiloxParticle& p, uint32_t mh, uint32_t ml) {
+    uint32_t c0, c1, c2, c3, h, l;
+    // round 0: c = (ctr, 0, 0, 0): c0 = 0 ^ 0 ^ K0 = pid_lo ; c1 = 0 ; c2 = hi(M0*ctr) ^ K1 ; c3 = lo(M0*ctr)
+    c2 = mh ^ p.k1[0];
+    c3 = ml;
+    // round 1: p0 = M0*pid_lo (hoisted), p1 = M1*c2
+    mulhilo(PHILOX_M1, c2, h, l);
+    c0 = h ^ p.k0[1];  // c1 == 0
+    c1 = l;
+    c2 = c3 ^ p.q1;
+    // round 2: c3 == p0lo (hoisted) is folded into r2
+    {
+        uint32_t h0, l0, h1, l1;
+        mulhilo(PHILOX_M0, c0, h0, l0);
+        mulhilo(PHILOX_M1, c2, h1, l1);
+        c0 = h1 ^ c1 ^ p.k0[2];
+        c1 = l1;
+        c2 = h0 ^ p.r2;
+        c3 = l0;
+    }
+#pragma unroll
+    for (int r = 3; r < 10; r++) philox_round(c0, c1, c2, c3, p.k0[r], p.k1[r]);
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// ---------------------------------------------------------------------------
+// Threefry4x32-20 (generators.py:125-154)
+// ---------------------------------------------------------------------------
+// Rotation pairs R[r % 8] (generators.py:44-47) as compile-time constants.
+template <int R> struct TfRot;
+template <> struct TfRot<0> { static constexpr int a = 10, b = 26; };
+template <> struct TfRot<1> { static constexpr int a = 11, b = 21; };
+template <> struct TfRot<2> { static constexpr int a = 13, b = 27; };
+template <> struct TfRot<3> { static constexpr int a = 23, b = 5; };
+template <> struct TfRot<4> { static constexpr int a = 6, b = 20; };
+template <> struct TfRot<5> { static constexpr int a = 17, b = 11; };
+template <> struct TfRot<6> { static constexpr int a = 25, b = 10; };
+template <> struct TfRot<7> { static constexpr int a = 18, b = 20; };
+
+template <int R>
+__host__ __device__ __forceinline__ void threefry_round(uint32_t& x0, uint32_t& x1, uint32_t& x2, uint32_t& x3) {
+    constexpr int ra = TfRot<R % 8>::a, rb = TfRot<R % 8>::b;
+    if (R % 2 == 0) {
+        x0 += x1; x1 = rotl32(x1, ra) ^ x0;
+        x2 += x3; x3 = rotl32(x3, rb) ^ x2;
+    } else {
+        x0 += x3; x3 = rotl32(x3, ra) ^ x0;
+        x2 += x1; x1 = rotl32(x1, rb) ^ x2;
+    }
+}
+
+// Key injection j (after round 4j-1): x[i] += ks[(j+i)%5]; x3 += j.
+template <int J>
+__host__ __device__ __forceinline__ void threefry_inject(uint32_t& x0, uint32_t& x1, uint32_t& x2, uint32_t& x3,
+                                                         const uint32_t ks[5]) {
+    x0 += ks[(J + 0) % 5];
+    x1 += ks[(J + 1) % 5];
+    x2 += ks[(J + 2) % 5];
+    x3 += ks[(J + 3) % 5] + (uint32_t)J;
+}
+
+// Rounds FIRST..19 with injections, starting from state x (already past rounds < FIRST).
+template <int FIRST>
+__host__ __device__ __forceinline__ void threefry_rounds_from(uint32_t& x0, uint32_t& x1, uint32_t& x2, uint32_t& x3,
+                                                              const uint32_t ks[5]) {
+#define TF_R(R)                                                         \
+    if (R >= FIRST) {                                                   \
+        threefry_round<R>(x0, x1, x2, x3);                              \
+        if ((R + 1) % 4 == 0) threefry_inject<(R + 1) / 4>(x0, x1, x2, x3, ks); \
+    }
+    TF_R(0) TF_R(1) TF_R(2) TF_R(3) TF_R(4) TF_R(5) TF_R(6) TF_R(7) TF_R(8) TF_R(9)
+    TF_R(10) TF_R(11) TF_R(12) TF_R(13) TF_R(14) TF_R(15) TF_R(16) TF_R(17) TF_R(18) TF_R(19)
+#undef TF_R
+}
+
+__host__ __device__ __forceinline__ uint4 threefry_block(uint4 c, uint32_t k0, uint32_t k1, uint32_t k2, uint32_t k3) {
+    uint32_t ks[5] = {k0, k1, k2, k3, THREEFRY_PARITY ^ k0 ^ k1 ^ k2 ^ k3};
+    uint32_t x0 = c.x + ks[0], x1 = c.y + ks[1], x2 = c.z + ks[2], x3 = c.w + ks[3];
+    threefry_rounds_from<0>(x0, x1, x2, x3, ks);
+    return make_uint4(x0, x1, x2, x3);
+}
+
+// Variable round count (the reference's `rounds=` argument, used by the
+// 13-round Random123 KAT). Not a hot path.
+__host__ __device__ inline uint4 threefry_block_rounds(uint4 c, const uint32_t key[4], int rounds) {
+    uint32_t ks[5] = {key[0], key[1], key[2], key[3], THREEFRY_PARITY ^ key[0] ^ key[1] ^ key[2] ^ key[3]};
+    uint32_t x[4] = {c.x + ks[0], c.y + ks[1], c.z + ks[2], c.w + ks[3]};
+    const int ROT[8][2] = {{10, 26}, {11, 21}, {13, 27}, {23, 5}, {6, 20}, {17, 11}, {25, 10}, {18, 20}};
+    for (int r = 0; r < rounds; r++) {
+        int ra = ROT[r % 8][0], rb = ROT[r % 8][1];
+        int a = (r % 2 == 0) ? 1 : 3, b = (r % 2 == 0) ? 3 : 1;
+        x[0] += x[a]; x[a] = rotl32(x[a], ra) ^ x[0];
+        x[2] += x[b]; x[b] = rotl32(x[b], rb) ^ x[2];
+        if ((r + 1) % 4 == 0) {
+            uint32_t j = (uint32_t)((r + 1) / 4);
+            for (int i = 0; i < 4; i++) x[i] += ks[(j + i) % 5];
+            x[3] += j;
+        }
+    }
+    return make_uint4(x[0], x[1], x[2], x[3]);
+}
+
+// Single stream: key (k0, k1, sc, 0), ctr (bc, 0, 0, 0). Rounds 0-1 are mostly
+// launch-uniform; the host folds them.
+struct ThreefryStream {
+    uint32_t ks[5];
+    uint32_t s01;   // ks0 + ks1: round 0 x0 = bc + s01
+    uint32_t r1;    // rotl(ks1, 10): round 0 x1 = r1 ^ x0
+    uint32_t x2_0;  // ks2 + ks3 (round 0 x2)
+    uint32_t x3_0;  // rotl(ks3, 26) ^ x2_0 (round 0 x3)
+    uint32_t x3r;   // rotl(x3_0, 11) (round 1)
+};
+
+inline ThreefryStream threefry_stream_setup(uint64_t seed, uint32_t sc) {
+    ThreefryStream p;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32), k2 = sc, k3 = 0;
+    p.ks[0] = k0; p.ks[1] = k1; p.ks[2] = k2; p.ks[3] = k3;
+    p.ks[4] = THREEFRY_PARITY ^ k0 ^ k1 ^ k2 ^ k3;
+    p.s01 = p.ks[0] + p.ks[1];
+    p.r1 = rotl32(p.ks[1], 10);
+    p.x2_0 = p.ks[2] + p.ks[3];
+    p.x3_0 = rotl32(p.ks[3], 26) ^ p.x2_0;
+    p.x3r = rotl32(p.x3_0, 11);
+    return p;
+}
+
+__device__ __forceinline__ uint4 threefry_stream_block(const ThreefryStream& p, uint32_t bc) {
+    // round 0 (even; rot 10, 26): x = (bc+ks0, ks1, ks2, ks3)
+    uint32_t x0 = bc + p.s01;
+    uint32_t x1 = p.r1 ^ x0;
+    // x2 = x2_0, x3 = x3_0 (uniform)
+    // round 1 (odd; rot 11, 21)
+    x0 += p.x3_0;
+    uint32_t x3 = p.x3r ^ x0;
+    uint32_t x2 = p.x2_0 + x1;
+    x1 = rotl32(x1, 21) ^ x2;
+    threefry_rounds_from<2>(x0, x1, x2, x3, p.ks);
+    return make_uint4(x0, x1, x2, x3);
+}
+
+// ---------------------------------------------------------------------------
+// Squares (generators.py:157-187)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t squares_key(uint64_t seed) {
+    uint64_t s = seed & 0xFFFFFFFFull;
+    uint64_t z = s + GOLDEN64;
+    z = (z ^ (z >> 30)) * SPLITMIX_M1;
+    z = (z ^ (z >> 27)) * SPLITMIX_M2;
+    z ^= z >> 31;
+    return (z ^ (s << 32)) | 1ull;
+}
+
+__host__ __device__ __forceinline__ uint64_t swap32(uint64_t x) { return (x >> 32) | (x << 32); }
+
+__host__ __device__ __forceinline__ uint32_t squares_round(uint64_t key, uint64_t ctr) {
+    uint64_t x = ctr * key, y = x, z = y + key;
+    x = swap32(x * x + y);
+    x = swap32(x * x + z);
+    x = swap32(x * x + y);
+    return (uint32_t)((x * x + z) >> 32);
+}
+
+// Single stream: ctr = (sc << 32) | bc, so ctr*key = bc*key + ((sc*key_lo) << 32).
+struct SquaresStream {
+    uint64_t key;
+    uint64_t base;  // (sc*key) mod 2^64 restricted to the sc<<32 term: (sc*key_lo) << 32
+};
+
+inline SquaresStream squares_stream_setup(uint64_t seed, uint32_t sc) {
+    SquaresStream p;
+    p.key = squares_key(seed);
+    p.base = ((uint64_t)sc << 32) * p.key;
+    return p;
+}
+
+__device__ __forceinline__ uint32_t squares_stream_word(const SquaresStream& p, uint32_t bc) {
+    uint64_t x = (uint64_t)bc * p.key + p.base, y = x, z = y + p.key;
+    x = swap32(x * x + y);
+    x = swap32(x * x + z);
+    x = swap32(x * x + y);
+    return (uint32_t)((x * x + z) >> 32);
+}
+
+// ---------------------------------------------------------------------------
+// Tyche (generators.py:190-224)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ void tyche_mix(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d) {
+    a += b; d = rotl32(d ^ a, 16);
+    c += d; b = rotl32(b ^ c, 12);
+    a += b; d = rotl32(d ^ a, 8);
+    c += d; b = rotl32(b ^ c, 7);
+}
+
+__host__ __device__ __forceinline__ uint4 tyche_init(uint64_t seed, uint32_t sc) {
+    uint32_t a = (uint32_t)(seed >> 32), b = (uint32_t)seed, c = TYCHE_INIT_CONST, d = sc;
+#pragma unroll 4
+    for (int i = 0; i < 20; i++) tyche_mix(a, b, c, d);
+    return make_uint4(a, b, c, d);
+}
+
+// ---------------------------------------------------------------------------
+// Word -> variate maps (distributions.py:42-120), exact where the reference is.
+// ---------------------------------------------------------------------------
+// uniform_f32: (w >> 8) * 2^-24 (exact in float; the reference rounds
+// (w>>8)*2^-24 in double then casts, which is the same value).
+__device__ __forceinline__ float u32_to_f32(uint32_t w) { return (float)(w >> 8) * 0x1p-24f; }
+
+// uniform_f64: ((lo | hi<<32) >> 11) * 2^-53, low word first.
+__device__ __forceinline__ double u32x2_to_f64(uint32_t lo, uint32_t hi) {
+    uint64_t u = ((uint64_t)hi << 32) | lo;
+    return (double)(u >> 11) * 0x1p-53;
+}
+
+// Box-Muller (distributions.py:72-81, :110-120): u1 = 1 - f64(w0,w1), u2 = f64(w2,w3),
+// r = sqrt(-2 ln u1), (r cos(2pi u2), r sin(2pi u2)). The argument is the
+// ROUNDED product (2*pi)*u2, exactly as the reference forms it.
+__device__ __forceinline__ void box_muller(uint4 w, double& z0, double& z1) {
+    const double two_pi = 6.283185307179586;  // 2.0 * math.pi, rounded
+    double u1 = 1.0 - u32x2_to_f64(w.x, w.y);
+    double u2 = u32x2_to_f64(w.z, w.w);
+    double r = sqrt(-2.0 * log(u1));
+    double t = __dmul_rn(two_pi, u2);
+    double s, c;
+    sincos(t, &s, &c);
+    z0 = __dmul_rn(r, c);
+    z1 = __dmul_rn(r, s);
+}
+
+}  // namespace cbrng

@@ -1,0 +1,260 @@
+// cbrng_fill.cu — single-stream bulk fills: Generator.words and the fused
+// distribution fills (bulk.py:223-281, distributions.py:99-120).
+//
+// Layout: one "unit" = 4 consecutive words of the stream (one Philox/Threefry
+// block, or 4 Squares counters). Lane l of a warp owns units base + l + 32j
+// (j < ILP), so every store instruction of a warp writes one contiguous
+// 512-byte run (128-bit st.global.cs per lane) and each thread keeps ILP
+// independent cipher evaluations in flight. The grid is the resident grid
+// (SMs x CTAs/SM), persistent over the output.
+//
+// Counter arithmetic: the fill starts at stream word `word_pos`. For Philox/Threefry
+// that is block b0 = (word_pos >> 2) mod 2^32 (bulk.py:215-217) at word skip =
+// word_pos & 3; unit u is block (b0 + u) when skip == 0, otherwise the last
+// 4 - skip words of block b0 + u followed by the first skip words of block
+// b0 + u + 1 (a resumed, mid-block generator: 2 cipher calls per unit).
+// Squares word k of unit u uses counter (word_pos + 4u + k) mod 2^32 (bulk.py:268).
+#include "cbrng_internal.cuh"
+
+namespace cbrng {
+
+enum Out : int { OUT_U32 = 0, OUT_F32 = 1, OUT_F64 = 2, OUT_NORMAL = 3 };
+
+template <int ALG> struct StreamOf;
+template <> struct StreamOf<PHILOX> { using T = PhiloxStream; };
+template <> struct StreamOf<THREEFRY> { using T = ThreefryStream; };
+template <> struct StreamOf<SQUARES> { using T = SquaresStream; };
+
+template <int ALG>
+struct FillArgs {
+    typename StreamOf<ALG>::T p;
+    uint32_t bc0;
+    uint32_t skip;     // 0..3: words of block bc0 already consumed (Philox/Threefry)
+    uint32_t tail;     // trailing output elements after the last full unit
+    uint64_t n_units;  // full units
+    void *out0;
+    void *out1;
+};
+
+template <int ALG>
+__device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, uint32_t bc) {
+    if constexpr (ALG == PHILOX) return philox_stream_block(p, bc);
+    else return threefry_stream_block(p, bc);
+}
+
+template <int ALG, bool SKIP>
+__device__ __forceinline__ uint4 unit_words(const typename StreamOf<ALG>::T &p, uint32_t bc0, uint32_t skip, uint64_t u) {
+    if constexpr (ALG == SQUARES) {
+        uint32_t c = bc0 + 4u * (uint32_t)u;
+        return make_uint4(squares_stream_word(p, c), squares_stream_word(p, c + 1),
+                          squares_stream_word(p, c + 2), squares_stream_word(p, c + 3));
+    } else if constexpr (!SKIP) {
+        return block_at<ALG>(p, bc0 + (uint32_t)u);
+    } else {
+        uint4 a = block_at<ALG>(p, bc0 + (uint32_t)u), b = block_at<ALG>(p, bc0 + (uint32_t)u + 1);
+        if (skip == 1) return make_uint4(a.y, a.z, a.w, b.x);
+        if (skip == 2) return make_uint4(a.z, a.w, b.x, b.y);
+        return make_uint4(a.w, b.x, b.y, b.z);
+    }
+}
+
+template <int OUT>
+__device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w) {
+    if constexpr (OUT == OUT_U32) {
+        __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
+    } else if constexpr (OUT == OUT_F32) {
+        __stcs(reinterpret_cast<float4 *>(out0) + u,
+               make_float4(u32_to_f32(w.x), u32_to_f32(w.y), u32_to_f32(w.z), u32_to_f32(w.w)));
+    } else if constexpr (OUT == OUT_F64) {
+        __stcs(reinterpret_cast<double2 *>(out0) + u, make_double2(u32x2_to_f64(w.x, w.y), u32x2_to_f64(w.z, w.w)));
+    } else {
+        double z0, z1;
+        box_muller(w, z0, z1);
+        __stcs(reinterpret_cast<double *>(out0) + u, z0);
+        __stcs(reinterpret_cast<double *>(out1) + u, z1);
+    }
+}
+
+// Partial trailing unit (1-3 words, or 1 double): element-wise stores.
+template <int OUT>
+__device__ __forceinline__ void store_tail(void *out0, uint64_t u, uint32_t tail, uint4 w) {
+    uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    if constexpr (OUT == OUT_U32) {
+        for (uint32_t k = 0; k < tail; k++) reinterpret_cast<uint32_t *>(out0)[4 * u + k] = ws[k];
+    } else if constexpr (OUT == OUT_F32) {
+        for (uint32_t k = 0; k < tail; k++) reinterpret_cast<float *>(out0)[4 * u + k] = u32_to_f32(ws[k]);
+    } else if constexpr (OUT == OUT_F64) {
+        if (tail) reinterpret_cast<double *>(out0)[2 * u] = u32x2_to_f64(w.x, w.y);
+    }
+}
+
+template <int ALG, int OUT, int ILP, bool SKIP>
+__global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr uint32_t TILE = 32 * ILP;
+    for (uint64_t base = warp * TILE; base < a.n_units; base += nwarps * TILE) {
+        uint4 w[ILP];
+#pragma unroll
+        for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP>(a.p, a.bc0, a.skip, base + lane + 32 * j);
+#pragma unroll
+        for (int j = 0; j < ILP; j++) {
+            uint64_t u = base + lane + 32 * j;
+            if (u < a.n_units) store_unit<OUT>(a.out0, a.out1, u, w[j]);
+        }
+    }
+    if (a.tail && blockIdx.x == 0 && threadIdx.x == 0) {
+        store_tail<OUT>(a.out0, a.n_units, a.tail, unit_words<ALG, SKIP>(a.p, a.bc0, a.skip, a.n_units));
+    }
+}
+
+// Tyche is sequential within a stream (generators.py:221-224; _kernels.py:3-5):
+// one thread walks the chain. Latency-bound (~12 dependent ALU ops per word).
+template <int OUT>
+__global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1, uint32_t *state_out) {
+    uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
+    for (uint64_t i = 0; i < n; i++) {
+        if constexpr (OUT == OUT_U32) {
+            tyche_mix(a, b, c, d);
+            reinterpret_cast<uint32_t *>(out0)[i] = b;
+        } else if constexpr (OUT == OUT_F32) {
+            tyche_mix(a, b, c, d);
+            reinterpret_cast<float *>(out0)[i] = u32_to_f32(b);
+        } else if constexpr (OUT == OUT_F64) {
+            tyche_mix(a, b, c, d);
+            uint32_t lo = b;
+            tyche_mix(a, b, c, d);
+            reinterpret_cast<double *>(out0)[i] = u32x2_to_f64(lo, b);
+        } else {
+            uint4 w;
+            tyche_mix(a, b, c, d); w.x = b;
+            tyche_mix(a, b, c, d); w.y = b;
+            tyche_mix(a, b, c, d); w.z = b;
+            tyche_mix(a, b, c, d); w.w = b;
+            double z0, z1;
+            box_muller(w, z0, z1);
+            reinterpret_cast<double *>(out0)[i] = z0;
+            reinterpret_cast<double *>(out1)[i] = z1;
+        }
+    }
+    if (state_out) {
+        state_out[0] = a; state_out[1] = b; state_out[2] = c; state_out[3] = d;
+    }
+}
+
+constexpr int FILL_BLOCK = 256;
+
+template <int ALG, int OUT, bool SKIP>
+static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
+    constexpr int ILP = 2;
+    auto k = fill_kernel<ALG, OUT, ILP, SKIP>;
+    uint64_t work = (a.n_units + (FILL_BLOCK * ILP) - 1) / (FILL_BLOCK * ILP);
+    unsigned grid = grid_for(k, FILL_BLOCK, 0, work ? work : 1);
+    k<<<grid, FILL_BLOCK, 0, st>>>(a);
+    return check_launch("fill_kernel");
+}
+
+template <int ALG, int OUT>
+static int launch_fill(uint64_t seed, uint32_t sc, uint64_t word_pos, uint64_t n_units, uint32_t tail, void *out0,
+                       void *out1, cudaStream_t st) {
+    if (n_units == 0 && tail == 0) return CBRNG_OK;
+    FillArgs<ALG> a;
+    if constexpr (ALG == PHILOX) a.p = philox_stream_setup(seed, sc);
+    else if constexpr (ALG == THREEFRY) a.p = threefry_stream_setup(seed, sc);
+    else a.p = squares_stream_setup(seed, sc);
+    if constexpr (ALG == SQUARES) {
+        a.bc0 = (uint32_t)word_pos;
+        a.skip = 0;
+    } else {
+        a.bc0 = (uint32_t)(word_pos >> 2);
+        a.skip = (uint32_t)(word_pos & 3);
+    }
+    a.tail = tail;
+    a.n_units = n_units;
+    a.out0 = out0;
+    a.out1 = out1;
+    if (ALG != SQUARES && a.skip) return launch_fill_k<ALG, OUT, true>(a, st);
+    return launch_fill_k<ALG, OUT, false>(a, st);
+}
+
+template <int OUT>
+static int dispatch_fill(int alg, uint64_t seed, uint32_t sc, uint64_t word_pos, const uint32_t *tyche_state,
+                         uint64_t n_elems, void *out0, void *out1, uint32_t *tyche_state_out, void *stream) {
+    CBRNG_CHECK_ALG(alg);
+    clear_error();
+    cudaStream_t st = as_stream(stream);
+    if (alg == TYCHE) {
+        CBRNG_REQUIRE(tyche_state != nullptr, "tyche fills need the serial state (tyche_state)");
+        uint4 s = make_uint4(tyche_state[0], tyche_state[1], tyche_state[2], tyche_state[3]);
+        if (n_elems == 0 && tyche_state_out == nullptr) return CBRNG_OK;
+        tyche_stream_kernel<OUT><<<1, 1, 0, st>>>(s, n_elems, out0, out1, tyche_state_out);
+        return check_launch("tyche_stream_kernel");
+    }
+    if (alg == SQUARES) seed &= 0xFFFFFFFFull;  // generators.py:256-257
+    // elements per 4-word unit: u32/f32 4, f64 2, normal pairs 1
+    const uint64_t per = (OUT == OUT_U32 || OUT == OUT_F32) ? 4 : (OUT == OUT_F64 ? 2 : 1);
+    const size_t align = (OUT == OUT_NORMAL) ? 8 : 16;
+    if (n_elems >= per) {
+        if (!aligned(out0, align) || (out1 && !aligned(out1, align))) {
+            set_error("output pointer not %zu-byte aligned", align);
+            return CBRNG_EALIGN;
+        }
+    }
+    uint64_t n_units = n_elems / per;
+    uint32_t tail = (uint32_t)(n_elems % per);
+    switch (alg) {
+        case PHILOX: return launch_fill<PHILOX, OUT>(seed, sc, word_pos, n_units, tail, out0, out1, st);
+        case THREEFRY: return launch_fill<THREEFRY, OUT>(seed, sc, word_pos, n_units, tail, out0, out1, st);
+        default: return launch_fill<SQUARES, OUT>(seed, sc, word_pos, n_units, tail, out0, out1, st);
+    }
+}
+
+}  // namespace cbrng
+
+using namespace cbrng;
+
+extern "C" {
+
+int cbrng_words(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos, const uint32_t *tyche_state,
+                uint64_t n, uint32_t *out, uint32_t *tyche_state_out, void *stream) {
+    return dispatch_fill<OUT_U32>(alg, seed, stream_ctr, word_pos, tyche_state, n, out, nullptr, tyche_state_out,
+                                  stream);
+}
+
+int cbrng_uniform_f32(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos, const uint32_t *tyche_state,
+                      uint64_t n, float *out, uint32_t *tyche_state_out, void *stream) {
+    return dispatch_fill<OUT_F32>(alg, seed, stream_ctr, word_pos, tyche_state, n, out, nullptr, tyche_state_out,
+                                  stream);
+}
+
+int cbrng_uniform_f64(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos, const uint32_t *tyche_state,
+                      uint64_t n, double *out, uint32_t *tyche_state_out, void *stream) {
+    return dispatch_fill<OUT_F64>(alg, seed, stream_ctr, word_pos, tyche_state, n, out, nullptr, tyche_state_out,
+                                  stream);
+}
+
+int cbrng_normal2_f64(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos, const uint32_t *tyche_state,
+                      uint64_t n_pairs, double *z0, double *z1, uint32_t *tyche_state_out, void *stream) {
+    return dispatch_fill<OUT_NORMAL>(alg, seed, stream_ctr, word_pos, tyche_state, n_pairs, z0, z1,
+                                     tyche_state_out, stream);
+}
+
+int cbrng_tyche_fill(uint64_t *state, uint64_t n, uint32_t *out, void *stream) {
+    CBRNG_REQUIRE(state != nullptr, "state is NULL");
+    uint32_t s[4] = {(uint32_t)state[0], (uint32_t)state[1], (uint32_t)state[2], (uint32_t)state[3]};
+    uint32_t *dev_state = nullptr;
+    cudaStream_t st = as_stream(stream);
+    int rc = check_cuda(cudaMallocAsync(&dev_state, 16, st), "cudaMallocAsync");
+    if (rc) return rc;
+    rc = cbrng_words(TYCHE, 0, 0, 0, s, n, out, dev_state, stream);
+    uint32_t back[4] = {s[0], s[1], s[2], s[3]};
+    if (rc == 0) rc = check_cuda(cudaMemcpyAsync(back, dev_state, 16, cudaMemcpyDeviceToHost, st), "copy state");
+    cudaFreeAsync(dev_state, st);
+    if (rc == 0) rc = check_cuda(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (rc == 0)
+        for (int i = 0; i < 4; i++) state[i] = back[i];
+    return rc;
+}
+
+}  // extern "C"

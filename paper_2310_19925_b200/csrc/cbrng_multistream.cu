@@ -1,0 +1,348 @@
+// cbrng_multistream.cu — many streams at once: bulk.prefix_words (bulk.py:162-207),
+// _kernels.philox_block_lanes (_kernels.py:54-86) and the vector block functions
+// (bulk.py:49-159).
+//
+// Output is row-major out[stream][word] exactly as the reference returns it.
+// Counter-based algorithms (Philox/Threefry/Squares) are random access in both
+// axes, so lanes are mapped to contiguous 16-byte chunks of the output:
+//   * rows of >= 128 words: one warp per row, lane l takes chunks l, l+32, ...
+//     (the per-stream key schedule is hoisted out of the chunk loop);
+//   * shorter rows: a warp covers floor(32 / chunks_per_row) whole rows per pass.
+// Either way each warp store instruction writes one contiguous run.
+// Tyche is serial within a stream (bulk.py:9-11): one thread per stream, and a
+// warp transposes its 32 streams x 32 words through padded shared memory so the
+// global stores are full 128-byte lines.
+#include "cbrng_internal.cuh"
+
+namespace cbrng {
+
+struct PrefixArgs {
+    const uint64_t *seeds;
+    uint64_t seed_base;
+    const uint32_t *ctrs;
+    uint32_t ctr_scalar;
+    uint32_t nwords;
+    uint64_t n_streams;
+    void *out;
+};
+
+__device__ __forceinline__ uint64_t seed_of(const PrefixArgs &a, uint64_t i) {
+    return a.seeds ? a.seeds[i] : a.seed_base + i;
+}
+__device__ __forceinline__ uint32_t ctr_of(const PrefixArgs &a, uint64_t i) {
+    return a.ctrs ? a.ctrs[i] : a.ctr_scalar;
+}
+
+// Per-stream key material for the counter-based algorithms.
+template <int ALG> struct StreamKey;
+template <> struct StreamKey<PHILOX> {
+    uint32_t k0, k1, sc;
+    __device__ __forceinline__ StreamKey(uint64_t seed, uint32_t c) : k0((uint32_t)seed), k1((uint32_t)(seed >> 32)), sc(c) {}
+    __device__ __forceinline__ uint4 block(uint32_t b) const { return philox_block(make_uint4(sc, b, 0, 0), k0, k1); }
+};
+template <> struct StreamKey<THREEFRY> {
+    uint32_t k0, k1, sc;
+    __device__ __forceinline__ StreamKey(uint64_t seed, uint32_t c) : k0((uint32_t)seed), k1((uint32_t)(seed >> 32)), sc(c) {}
+    __device__ __forceinline__ uint4 block(uint32_t b) const { return threefry_block(make_uint4(b, 0, 0, 0), k0, k1, sc, 0); }
+};
+template <> struct StreamKey<SQUARES> {
+    uint64_t key, base;
+    __device__ __forceinline__ StreamKey(uint64_t seed, uint32_t c) {
+        key = squares_key(seed);
+        base = ((uint64_t)c << 32) * key;
+    }
+    __device__ __forceinline__ uint32_t word(uint32_t j) const {
+        uint64_t x = (uint64_t)j * key + base, y = x, z = y + key;
+        x = swap32(x * x + y);
+        x = swap32(x * x + z);
+        x = swap32(x * x + y);
+        return (uint32_t)((x * x + z) >> 32);
+    }
+    __device__ __forceinline__ uint4 block(uint32_t b) const {
+        uint32_t j = 4 * b;
+        return make_uint4(word(j), word(j + 1), word(j + 2), word(j + 3));
+    }
+};
+
+template <int ALG>
+__device__ __forceinline__ uint32_t single_word(const StreamKey<ALG> &k, uint32_t j) {
+    if constexpr (ALG == SQUARES) {
+        return k.word(j);
+    } else {
+        uint4 b = k.block(j >> 2);
+        uint32_t r = b.x;
+        r = ((j & 3) == 1) ? b.y : r;
+        r = ((j & 3) == 2) ? b.z : r;
+        r = ((j & 3) == 3) ? b.w : r;
+        return r;
+    }
+}
+
+// OUT: 0 = u32 words, 1 = uniform f32.
+template <int OUT>
+__device__ __forceinline__ void store4(void *out, uint64_t word_index, uint4 w) {
+    if constexpr (OUT == 0) {
+        __stcs(reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(out) + word_index), w);
+    } else {
+        __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + word_index),
+               make_float4(u32_to_f32(w.x), u32_to_f32(w.y), u32_to_f32(w.z), u32_to_f32(w.w)));
+    }
+}
+template <int OUT>
+__device__ __forceinline__ void store1(void *out, uint64_t word_index, uint32_t w) {
+    if constexpr (OUT == 0) reinterpret_cast<uint32_t *>(out)[word_index] = w;
+    else reinterpret_cast<float *>(out)[word_index] = u32_to_f32(w);
+}
+
+// CW = words per chunk: 4 (nwords % 4 == 0, 16-byte stores) or 1 (generic).
+template <int ALG, int OUT, int CW>
+__global__ void __launch_bounds__(256) prefix_kernel(const __grid_constant__ PrefixArgs a) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t cpr = a.nwords / CW;  // chunks per row
+    if (cpr >= 32) {
+        for (uint64_t row = warp; row < a.n_streams; row += nwarps) {
+            const StreamKey<ALG> k(seed_of(a, row), ctr_of(a, row));
+            const uint64_t rbase = row * a.nwords;
+            for (uint32_t j = lane; j < cpr; j += 32) {
+                if constexpr (CW == 4) store4<OUT>(a.out, rbase + 4ull * j, k.block(j));
+                else store1<OUT>(a.out, rbase + j, single_word<ALG>(k, j));
+            }
+        }
+    } else {
+        const uint32_t rpp = 32 / cpr;  // rows per pass
+        const uint32_t roff = lane / cpr, ch = lane - roff * cpr;
+        if (roff >= rpp) return;
+        for (uint64_t r0 = warp * rpp; r0 < a.n_streams; r0 += nwarps * rpp) {
+            const uint64_t row = r0 + roff;
+            if (row >= a.n_streams) break;
+            const StreamKey<ALG> k(seed_of(a, row), ctr_of(a, row));
+            if constexpr (CW == 4) store4<OUT>(a.out, row * a.nwords + 4ull * ch, k.block(ch));
+            else store1<OUT>(a.out, row * a.nwords + ch, single_word<ALG>(k, ch));
+        }
+    }
+}
+
+constexpr int TY_WARPS = 8;  // 256 threads
+constexpr int TY_PAD = 9;    // 8 x 16-byte chunks + 1 pad = 144-byte rows: conflict-free STS.128/LDS.128
+
+template <int OUT>
+__global__ void __launch_bounds__(256) tyche_prefix_kernel(const __grid_constant__ PrefixArgs a) {
+    __shared__ uint4 tile[TY_WARPS][32][TY_PAD];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t groups = a.nwords / 32, rem = a.nwords % 32;
+    for (uint64_t s0 = warp * 32; s0 < a.n_streams; s0 += nwarps * 32) {
+        const uint64_t sid = s0 + lane;
+        const bool valid = sid < a.n_streams;
+        uint4 st = tyche_init(valid ? seed_of(a, sid) : 0, valid ? ctr_of(a, sid) : 0);
+        uint32_t A = st.x, B = st.y, C = st.z, D = st.w;
+        for (uint32_t g = 0; g < groups; g++) {
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                uint4 w;
+                tyche_mix(A, B, C, D); w.x = B;
+                tyche_mix(A, B, C, D); w.y = B;
+                tyche_mix(A, B, C, D); w.z = B;
+                tyche_mix(A, B, C, D); w.w = B;
+                tile[wib][lane][c] = w;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const uint32_t r = k * 4 + (lane >> 3), c = lane & 7;
+                if (s0 + r < a.n_streams) store4<OUT>(a.out, (s0 + r) * a.nwords + g * 32 + c * 4, tile[wib][r][c]);
+            }
+            __syncwarp();
+        }
+        for (uint32_t j = 0; j < rem; j++) {
+            tyche_mix(A, B, C, D);
+            if (valid) store1<OUT>(a.out, sid * a.nwords + groups * 32 + j, B);
+        }
+    }
+}
+
+template <int ALG, int OUT>
+static int launch_prefix(const PrefixArgs &a, cudaStream_t st) {
+    if (a.nwords % 4 == 0) {
+        auto k = prefix_kernel<ALG, OUT, 4>;
+        uint64_t chunks = a.n_streams * (a.nwords / 4);
+        k<<<grid_for(k, 256, 0, (chunks + 255) / 256), 256, 0, st>>>(a);
+    } else {
+        auto k = prefix_kernel<ALG, OUT, 1>;
+        uint64_t chunks = a.n_streams * a.nwords;
+        k<<<grid_for(k, 256, 0, (chunks + 255) / 256), 256, 0, st>>>(a);
+    }
+    return check_launch("prefix_kernel");
+}
+
+template <int OUT>
+static int dispatch_prefix(int alg, const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs,
+                           uint32_t ctr_scalar, uint64_t n_streams, uint32_t nwords, void *out, void *stream) {
+    CBRNG_CHECK_ALG(alg);
+    clear_error();
+    if (n_streams == 0 || nwords == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(out != nullptr, "out is NULL");
+    if (nwords % 4 == 0 && !aligned(out, 16)) {
+        set_error("output pointer not 16-byte aligned");
+        return CBRNG_EALIGN;
+    }
+    PrefixArgs a{seeds, seed_base, ctrs, ctr_scalar, nwords, n_streams, out};
+    cudaStream_t st = as_stream(stream);
+    switch (alg) {
+        case PHILOX: return launch_prefix<PHILOX, OUT>(a, st);
+        case THREEFRY: return launch_prefix<THREEFRY, OUT>(a, st);
+        case SQUARES: return launch_prefix<SQUARES, OUT>(a, st);
+        default: {
+            if (nwords >= 32 && !aligned(out, 16)) {
+                set_error("output pointer not 16-byte aligned");
+                return CBRNG_EALIGN;
+            }
+            auto k = tyche_prefix_kernel<OUT>;
+            k<<<grid_for(k, 256, 0, (n_streams + 255) / 256), 256, 0, st>>>(a);
+            return check_launch("tyche_prefix_kernel");
+        }
+    }
+}
+
+// ---------------- vector block functions ----------------
+__global__ void philox4x32_kernel(const uint32_t *ctr, const uint32_t *key, uint64_t n, uint32_t *out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint4 r = philox_block(make_uint4(ctr[i], ctr[n + i], ctr[2 * n + i], ctr[3 * n + i]), key[i], key[n + i]);
+        out[i] = r.x; out[n + i] = r.y; out[2 * n + i] = r.z; out[3 * n + i] = r.w;
+    }
+}
+
+__global__ void threefry4x32_kernel(const uint32_t *ctr, const uint32_t *key, int rounds, uint64_t n, uint32_t *out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint4 c = make_uint4(ctr[i], ctr[n + i], ctr[2 * n + i], ctr[3 * n + i]);
+        uint4 r;
+        if (rounds == 20) {
+            r = threefry_block(c, key[i], key[n + i], key[2 * n + i], key[3 * n + i]);
+        } else {
+            uint32_t k[4] = {key[i], key[n + i], key[2 * n + i], key[3 * n + i]};
+            r = threefry_block_rounds(c, k, rounds);
+        }
+        out[i] = r.x; out[n + i] = r.y; out[2 * n + i] = r.z; out[3 * n + i] = r.w;
+    }
+}
+
+__global__ void squares32_kernel(const uint64_t *ctr, const uint64_t *key, uint64_t n, uint32_t *out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = squares_round(key[i], ctr[i]);
+}
+
+__global__ void squares_keys_kernel(const uint64_t *seeds, uint64_t n, uint64_t *keys) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        keys[i] = squares_key(seeds[i]);
+}
+
+__global__ void tyche_mix_kernel(uint32_t *s, uint64_t n, uint32_t rounds) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t a = s[i], b = s[n + i], c = s[2 * n + i], d = s[3 * n + i];
+        for (uint32_t r = 0; r < rounds; r++) tyche_mix(a, b, c, d);
+        s[i] = a; s[n + i] = b; s[2 * n + i] = c; s[3 * n + i] = d;
+    }
+}
+
+__global__ void tyche_init_kernel(const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs, uint32_t ctr_scalar,
+                                  uint64_t n, uint32_t *s) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint4 t = tyche_init(seeds ? seeds[i] : seed_base + i, ctrs ? ctrs[i] : ctr_scalar);
+        s[i] = t.x; s[n + i] = t.y; s[2 * n + i] = t.z; s[3 * n + i] = t.w;
+    }
+}
+
+__global__ void philox_block_lanes_kernel(const uint64_t *seeds, const uint64_t *scs, uint64_t block_ctr, uint64_t n,
+                                          uint32_t *out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t s = seeds[i];
+        uint4 r = philox_block(make_uint4((uint32_t)scs[i], (uint32_t)block_ctr, 0, 0), (uint32_t)s, (uint32_t)(s >> 32));
+        reinterpret_cast<uint4 *>(out)[i] = r;
+    }
+}
+
+template <typename K>
+static unsigned lanes_grid(K k, uint64_t n) { return grid_for(k, 256, 0, (n + 255) / 256); }
+
+}  // namespace cbrng
+
+using namespace cbrng;
+
+extern "C" {
+
+int cbrng_prefix_words(int alg, const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs, uint32_t ctr_scalar,
+                       uint64_t n_streams, uint32_t nwords, uint32_t *out, void *stream) {
+    return dispatch_prefix<0>(alg, seeds, seed_base, ctrs, ctr_scalar, n_streams, nwords, out, stream);
+}
+
+int cbrng_prefix_uniform_f32(int alg, const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs,
+                             uint32_t ctr_scalar, uint64_t n_streams, uint32_t nvalues, float *out, void *stream) {
+    return dispatch_prefix<1>(alg, seeds, seed_base, ctrs, ctr_scalar, n_streams, nvalues, out, stream);
+}
+
+int cbrng_philox_block_lanes(const uint64_t *seeds, const uint64_t *stream_ctrs, uint64_t block_ctr, uint64_t n,
+                             uint32_t *out, void *stream) {
+    clear_error();
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(seeds && stream_ctrs && out, "NULL pointer");
+    if (!aligned(out, 16)) { set_error("out not 16-byte aligned"); return CBRNG_EALIGN; }
+    philox_block_lanes_kernel<<<lanes_grid(philox_block_lanes_kernel, n), 256, 0, as_stream(stream)>>>(
+        seeds, stream_ctrs, block_ctr, n, out);
+    return check_launch("philox_block_lanes_kernel");
+}
+
+int cbrng_philox4x32(const uint32_t *ctr, const uint32_t *key, uint64_t n, uint32_t *out, void *stream) {
+    clear_error();
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(ctr && key && out, "NULL pointer");
+    philox4x32_kernel<<<lanes_grid(philox4x32_kernel, n), 256, 0, as_stream(stream)>>>(ctr, key, n, out);
+    return check_launch("philox4x32_kernel");
+}
+
+int cbrng_threefry4x32(const uint32_t *ctr, const uint32_t *key, int rounds, uint64_t n, uint32_t *out, void *stream) {
+    clear_error();
+    CBRNG_REQUIRE(rounds >= 0, "rounds must be >= 0");
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(ctr && key && out, "NULL pointer");
+    threefry4x32_kernel<<<lanes_grid(threefry4x32_kernel, n), 256, 0, as_stream(stream)>>>(ctr, key, rounds, n, out);
+    return check_launch("threefry4x32_kernel");
+}
+
+int cbrng_squares32(const uint64_t *ctr, const uint64_t *key, uint64_t n, uint32_t *out, void *stream) {
+    clear_error();
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(ctr && key && out, "NULL pointer");
+    squares32_kernel<<<lanes_grid(squares32_kernel, n), 256, 0, as_stream(stream)>>>(ctr, key, n, out);
+    return check_launch("squares32_kernel");
+}
+
+int cbrng_squares_keys(const uint64_t *seeds, uint64_t n, uint64_t *keys, void *stream) {
+    clear_error();
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(seeds && keys, "NULL pointer");
+    squares_keys_kernel<<<lanes_grid(squares_keys_kernel, n), 256, 0, as_stream(stream)>>>(seeds, n, keys);
+    return check_launch("squares_keys_kernel");
+}
+
+int cbrng_tyche_mix(uint32_t *state, uint64_t n, uint32_t rounds, void *stream) {
+    clear_error();
+    if (n == 0 || rounds == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(state, "NULL pointer");
+    tyche_mix_kernel<<<lanes_grid(tyche_mix_kernel, n), 256, 0, as_stream(stream)>>>(state, n, rounds);
+    return check_launch("tyche_mix_kernel");
+}
+
+int cbrng_tyche_init(const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs, uint32_t ctr_scalar, uint64_t n,
+                     uint32_t *state, void *stream) {
+    clear_error();
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(state, "NULL pointer");
+    tyche_init_kernel<<<lanes_grid(tyche_init_kernel, n), 256, 0, as_stream(stream)>>>(seeds, seed_base, ctrs,
+                                                                                        ctr_scalar, n, state);
+    return check_launch("tyche_init_kernel");
+}
+
+}  // extern "C"

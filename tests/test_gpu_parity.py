@@ -1,0 +1,340 @@
+"""Parity of the sm_100a CUDA path with the reference, through the C ABI.
+
+Bar: bit-exact for every integer stream and exact float map; Box-Muller within
+4 ulp(max(|z|, 1)) of the oracle (glibc libm, bit-identical to the reference's
+scalar normal2 — tests/test_oracle.py). Expected values come from the golden
+fixtures frozen from the reference (tests/golden) and from the CPU oracle on
+the same seeded inputs. Mirrors the reference's own suites
+(pkg/tests/test_generators.py, test_distributions.py, test_brownian.py).
+"""
+
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import ALGS
+
+pytestmark = pytest.mark.gpu
+
+M32 = 0xFFFFFFFF
+BM_ULP = 4  # Box-Muller tolerance, in ulp(max(|z|, 1))
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def cb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2310_19925_b200 as cb
+
+    return cb
+
+
+def host(t):
+    import torch
+
+    return t.cpu().numpy() if isinstance(t, torch.Tensor) else np.asarray(t)
+
+
+class TestKnownAnswers:
+    def test_block_functions(self, cb, golden):
+        for ctr, key, out in golden["philox_kat"]:
+            assert tuple(cb.philox_block(key, ctr)) == tuple(out)
+        for ctr, key, out in golden["threefry_kat_20"]:
+            assert tuple(cb.threefry_block(key, ctr)) == tuple(out)
+        for ctr, key, out in golden["threefry_kat_13"]:
+            assert tuple(cb.threefry_block(key, ctr, rounds=13)) == tuple(out)
+        for seed, key, words in golden["squares_kat"]:
+            assert cb.squares_key(seed) == key
+            assert [cb.squares_round(key, c) for c in range(3)] == words
+        kat = golden["tyche_kat"]
+        st = cb.tyche_init(kat["seed"], kat["ctr"])
+        assert list(st) == kat["state"]
+        words = []
+        for _ in range(4):
+            w, st = cb.tyche_next(st)
+            words.append(w)
+        assert words == kat["words"]
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_stream_seed42_scalar_and_bulk(self, cb, golden, alg):
+        g = cb.make_generator(alg, 42, 0)
+        assert [g.next_u32() for _ in range(8)] == golden["stream_seed42"][alg]
+        assert host(cb.make_generator(alg, 42, 0).words(8)).tolist() == golden["stream_seed42"][alg]
+
+    def test_vector_ciphers(self, cb, golden_arrays):
+        from paper_2310_19925_b200 import bulk
+
+        c, k = golden_arrays["blk_ctr"], golden_arrays["blk_key"]
+        assert np.array_equal(np.stack(bulk.philox4x32(*c, k[0], k[1])), golden_arrays["blk_philox"])
+        assert np.array_equal(np.stack(bulk.threefry4x32(*c, *k)), golden_arrays["blk_threefry"])
+        assert np.array_equal(bulk.squares32(golden_arrays["blk_sq_ctr"], golden_arrays["blk_sq_key"]),
+                              golden_arrays["blk_squares"])
+        assert np.array_equal(bulk.squares_keys(golden_arrays["blk_sq_seeds"]), golden_arrays["blk_sq_keys_of_seeds"])
+        assert np.array_equal(np.stack(bulk.tyche_mix(*c)), golden_arrays["blk_tyche_state"])
+
+
+class TestSingleStream:
+    def test_cfg1_bit_exact(self, cb, golden):
+        """BASELINE.json configs[0]: Philox u32 fill 2^20, seed 42, ctr 0."""
+        w = host(cb.make_generator("philox", 42, 0).words(2**20))
+        assert sha(w) == golden["cfg1"]["sha256"]
+        assert int(w[0]) == golden["cfg1"]["first"] and int(w[-1]) == golden["cfg1"]["last"]
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_stream_digests(self, cb, golden, golden_arrays, alg):
+        for i, (s, c) in enumerate(golden["stream_pairs"]):
+            w = cb.make_generator(alg, s, c).words(65536 + 3, device="cpu")
+            assert isinstance(w, np.ndarray) and w.dtype == np.uint32
+            assert sha(w) == golden["stream_digests"][alg][i]
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_block_counter_wrap(self, cb, golden, golden_arrays, alg):
+        g = cb.make_generator(alg, 5, 6)
+        g._block_ctr = 2**32 - 3
+        w = host(g.words(200))
+        assert np.array_equal(w, golden_arrays[f"wrap_{alg}"])
+        assert g._block_ctr == golden["wrap"][alg]["block_ctr_after"]
+        assert g._cache_pos == golden["wrap"][alg]["cache_pos_after"]
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_mixed_scalar_bulk_state(self, cb, golden, alg):
+        """The reference's interleaving sequence (make_golden.py state_after)."""
+        g = cb.make_generator(alg, 0xFEEDFACE, 3)
+        seq = [g.next_u32() for _ in range(3)]
+        seq += host(g.words(130)).tolist()
+        seq += [g.next_u32() for _ in range(2)]
+        seq += host(g.words(1001)).tolist()
+        ref = golden["state_after"][alg]
+        assert sha(np.array(seq, dtype=np.uint32)) == ref["sha"]
+        assert g.state_bytes().hex() == ref["state_bytes"]
+        if alg == "tyche":
+            assert list(g._tyche_state) == ref["tyche_state"]
+
+    @pytest.mark.parametrize("alg", ALGS)
+    @pytest.mark.parametrize("split", [0, 1, 4, 7, 3731])
+    def test_serialize_restore(self, cb, oracle, alg, split):
+        straight = oracle.stream_words(alg, 0x1234567, 9, 5000)
+        g = cb.make_generator(alg, 0x1234567, 9)
+        head = host(g.words(split))
+        restored = cb.Generator.from_state_bytes(g.state_bytes())
+        tail = host(restored.words(5000 - split))
+        assert np.array_equal(np.concatenate([head, tail]), straight)
+
+    @pytest.mark.parametrize("alg", ["philox", "threefry"])
+    @pytest.mark.parametrize("skip", [1, 2, 3])
+    def test_resume_mid_block_all_maps(self, cb, oracle, alg, skip):
+        """A generator resumed mid-block fills through the 2-block kernel variant."""
+        ref = oracle.stream_words(alg, 77, 5, 4 * 5000 + 16)
+        for kind in ("words", "f32", "f64"):
+            g = cb.make_generator(alg, 77, 5)
+            [g.next_u32() for _ in range(skip)]
+            if kind == "words":
+                assert np.array_equal(host(g.words(4099)), ref[skip:skip + 4099])
+            elif kind == "f32":
+                assert np.array_equal(host(cb.uniform_f32_array(g, 4099)), oracle.words_to_f32(ref[skip:skip + 4099]))
+            elif skip % 2 == 0:
+                assert np.array_equal(host(cb.uniform_f64_array(g, 2049)), oracle.words_to_f64(ref[skip:skip + 4098]))
+            else:
+                got = host(cb.uniform_f64_array(g, 2049))
+                assert np.array_equal(got, oracle.words_to_f64(ref[skip:skip + 4098]))
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_edge_sizes(self, cb, oracle, alg):
+        for n in (0, 1, 2, 3, 4, 5, 127, 128, 129, 1023, 4097):
+            w = host(cb.make_generator(alg, 31337, 9).words(n))
+            assert np.array_equal(w, oracle.stream_words(alg, 31337, 9, n))
+
+    def test_negative_count_rejected(self, cb):
+        with pytest.raises(ValueError):
+            cb.make_generator("philox", 1, 0).words(-1)
+
+    def test_unknown_algorithm_rejected(self, cb):
+        with pytest.raises(ValueError):
+            cb.make_generator("mt19937", 1, 0)
+
+
+class TestDistributions:
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_uniform_f32_f64(self, cb, golden, golden_arrays, alg):
+        assert sha(host(cb.uniform_f32_array(cb.make_generator(alg, 42, 0), 2**20))) == golden["uniform_f32_2p20"][alg]
+        assert sha(host(cb.uniform_f64_array(cb.make_generator(alg, 42, 0), 2**19))) == golden["uniform_f64_2p19"][alg]
+        assert np.array_equal(host(cb.uniform_f32_array(cb.make_generator(alg, 99, 2), 1029)), golden_arrays[f"uf32_{alg}"])
+        assert np.array_equal(host(cb.uniform_f64_array(cb.make_generator(alg, 99, 2), 1029)), golden_arrays[f"uf64_{alg}"])
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_normal2_within_tolerance(self, cb, oracle, golden_arrays, alg):
+        z0, z1 = (host(z) for z in cb.normal2_array(cb.make_generator(alg, 42, 0), 4099))
+        ref = golden_arrays[f"n2scalar_{alg}"]
+        for got, r in ((z0, ref[:, 0]), (z1, ref[:, 1])):
+            ulps = np.abs(got - r) / np.spacing(np.maximum(np.abs(r), 1.0))
+            assert ulps.max() <= BM_ULP, ulps.max()
+
+    def test_normal2_large_vs_oracle(self, cb, oracle):
+        n = 1 << 20
+        z0, z1 = (host(z) for z in cb.normal2_array(cb.make_generator("philox", 42, 0), n))
+        r0, r1 = oracle.normal2("philox", 42, 0, n)
+        for got, r in ((z0, r0), (z1, r1)):
+            ulps = np.abs(got - r) / np.spacing(np.maximum(np.abs(r), 1.0))
+            assert ulps.max() <= BM_ULP, ulps.max()
+
+    def test_scalar_forms(self, cb, oracle):
+        g = cb.make_generator("threefry", 12, 0)
+        w = oracle.stream_words("threefry", 12, 0, 64)
+        u = cb.uniform_f64(g)
+        assert u == ((int(w[0]) | (int(w[1]) << 32)) >> 11) * 2.0**-53
+        assert cb.range_u32(g, 6) == (int(w[2]) * 6) >> 32
+        assert cb.fill_bytes(cb.make_generator("philox", 42, 0), 5) == oracle.stream_words("philox", 42, 0, 2).astype("<u4").tobytes()[:5]
+
+
+class TestPrefixWords:
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_random_streams(self, cb, golden_arrays, alg):
+        from paper_2310_19925_b200 import bulk
+
+        seeds, ctrs = golden_arrays["prefix_seeds"], golden_arrays["prefix_ctrs"]
+        for nw in (1, 4, 7, 19):
+            assert np.array_equal(host(bulk.prefix_words(alg, seeds, ctrs, nw)), golden_arrays[f"prefix_{alg}_{nw}"])
+        assert np.array_equal(host(bulk.prefix_words(alg, seeds, 9, 12)), golden_arrays[f"prefix_{alg}_scalarctr"])
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_arange_2p16_x256(self, cb, golden, alg):
+        from paper_2310_19925_b200 import bulk
+
+        w = host(bulk.prefix_words(alg, range(2**16), 0, 256))
+        assert sha(w) == golden["prefix_arange_2p16_256"][alg]
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_row_shapes(self, cb, oracle, alg):
+        from paper_2310_19925_b200 import bulk
+
+        for n, nw in ((1, 1), (33, 8), (100, 36), (65, 128), (7, 260), (1000, 33)):
+            got = host(bulk.prefix_words(alg, range(1000, 1000 + n), 3, nw))
+            assert np.array_equal(got, oracle.prefix_words_arange(alg, 1000, n, 3, nw))
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_prefix_uniform_f32(self, cb, oracle, alg):
+        from paper_2310_19925_b200 import bulk
+
+        got = host(bulk.prefix_uniform_f32(alg, range(4096), 0, 256))
+        ref = oracle.words_to_f32(oracle.prefix_words_arange(alg, 0, 4096, 0, 256).reshape(-1)).reshape(4096, 256)
+        assert np.array_equal(got, ref)
+
+    def test_philox_block_lanes(self, cb, golden_arrays, oracle):
+        from paper_2310_19925_b200 import bulk
+
+        seeds = golden_arrays["prefix_seeds"]
+        scs = golden_arrays["prefix_ctrs"].astype(np.uint64)
+        got = host(bulk.philox_block_lanes(seeds, scs, 3))
+        ref = oracle.prefix_words("philox", seeds, golden_arrays["prefix_ctrs"], 16)[:, 12:16]
+        assert np.array_equal(got, ref)
+
+
+class TestBrownian:
+    @pytest.mark.parametrize("alg", ALGS)
+    @pytest.mark.parametrize("mode", ["fused", "per_step"])
+    def test_checksum_1000x100(self, cb, golden, alg, mode):
+        r = cb.run_sim(cb.SimConfig(1000, 100, algorithm=alg, mode=mode))
+        assert str(r.checksum) == golden["brownian_1000x100"][alg]
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_cases_bit_exact(self, cb, golden, golden_arrays, alg):
+        for key, case in golden["brownian_cases"].items():
+            if not key.endswith("_" + alg):
+                continue
+            name = key[: -len(alg) - 1]
+            cfg = cb.SimConfig(**case["cfg"])
+            p0 = cb.init_particles(cfg)
+            for f in ("x", "y", "vx", "vy"):
+                assert np.array_equal(host(getattr(p0, f)), golden_arrays[f"bw_{name}_{alg}_init_{f}"])
+            r = cb.run_sim(cfg)
+            for f in ("x", "y", "vx", "vy"):
+                assert np.array_equal(host(getattr(r.particles, f)), golden_arrays[f"bw_{name}_{alg}_{f}"]), f
+            assert str(r.checksum) == case["checksum"]
+
+    def test_acceptance_c6_shape(self, cb, golden):
+        r = cb.run_sim(cb.SimConfig(100_000, 1000))
+        assert str(r.checksum) == golden["brownian_1e5x1e3_philox"]
+
+    def test_iteration_zero_rejected(self, cb):
+        cfg = cb.SimConfig(4, 1)
+        with pytest.raises(ValueError):
+            cb.apply_forces_step(cb.init_particles(cfg), 0, cfg)
+
+    def test_restart_matches_straight(self, cb, tmp_path):
+        full = cb.run_sim(cb.SimConfig(300, 20))
+        half = cb.run_sim(cb.SimConfig(300, 10, mode="per_step"))
+        snap = tmp_path / "half.snap"
+        cb.save_snapshot(snap, half.particles, next_iteration=11)
+        particles, next_it = cb.load_snapshot(snap)
+        resumed = cb.run_sim(cb.SimConfig(300, 10), particles=particles, start_iteration=next_it)
+        assert resumed.checksum == full.checksum
+
+    def test_shard_invariance_and_stats(self, cb):
+        """pid-range shards (any count) reproduce the single run bit for bit."""
+        import torch
+        from paper_2310_19925_b200 import brownian, sharding
+
+        cfg = cb.SimConfig(10_007, 50, algorithm="philox")
+        whole = cb.run_sim(cfg, with_checksum=False).particles
+        acc_whole = brownian.stats(whole)
+        for world in (2, 3, 8):
+            acc = torch.zeros(8, dtype=torch.int64, device="cuda")
+            xs = []
+            for r in range(world):
+                lo, hi = sharding.shard_range(cfg.n_particles, r, world)
+                p = brownian.init_particles(cfg, pid_base=lo, n=hi - lo)
+                brownian.run_steps(p, cfg)
+                brownian.stats(p, acc)
+                xs.append(p.x)
+            assert torch.equal(torch.cat(xs), whole.x)
+            assert torch.equal(acc, acc_whole)
+
+
+class TestSpotChecksAtScale:
+    """BASELINE configs at full size, checked by size-independent properties:
+    oracle spot checks at random positions and digest equality under sharding."""
+
+    @pytest.mark.parametrize("alg", ["philox", "threefry", "squares"])
+    def test_cfg2_uniform_f32_2p30_spot(self, cb, oracle, alg):
+        n = 1 << 30
+        out = cb.uniform_f32_array(cb.make_generator(alg, 42, 0), n)
+        rng = np.random.default_rng(5)
+        idx = np.concatenate([[0, 1, 2, 3, n - 4, n - 3, n - 2, n - 1], rng.integers(0, n // 4, 200) * 4])
+        for i in idx:
+            i = int(i) & ~3
+            if alg == "squares":
+                ref = oracle.words_to_f32(oracle.stream_words(alg, 42, 0, 4, block_ctr=i))
+            else:
+                ref = oracle.words_to_f32(oracle.stream_words(alg, 42, 0, 4, block_ctr=i // 4))
+            assert np.array_equal(out[i:i + 4].cpu().numpy(), ref), i
+        del out
+
+    def test_cfg5_multistream_sharded_digest(self, cb, oracle):
+        """100M-stream layout, shortened to 4M streams x 256: digest of the
+        whole == sum of shard digests; rows spot-checked against the oracle."""
+        import torch
+        from paper_2310_19925_b200 import bulk, sharding
+
+        n, nw = 1 << 22, 256
+        whole = bulk.prefix_words("philox", range(n), 0, nw)
+        d_whole = sharding.digest_words(whole, 0)
+        acc = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for r in range(4):
+            lo, hi = sharding.shard_range(n, r, 4)
+            part = bulk.prefix_words("philox", range(lo, hi), 0, nw)
+            sharding.digest_words(part, lo * nw, acc)
+        assert torch.equal(acc, d_whole)
+        for row in (0, 1, n // 2, n - 1):
+            assert np.array_equal(whole[row].cpu().numpy(), oracle.prefix_words_arange("philox", row, 1, 0, nw)[0])
+        small = whole[:1000].cpu().numpy()
+        assert sharding.digest_words_np(small.reshape(-1), 0) == int(
+            sharding.digest_words(whole[:1000], 0).cpu().numpy()[0]) % 2**64
