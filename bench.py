@@ -23,7 +23,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 from pathlib import Path
@@ -46,54 +45,67 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled every 5 ms by NVML during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.path = ROOT / "gpurun_out" / f"clocks_{os.getpid()}.csv"
+    def __init__(self, cuda_index: int):
+        import threading
+
+        self.cuda_index = cuda_index
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+        self.err = None
+
+    def _handle(self, nv):
+        import torch
+
+        try:
+            uuid = str(torch.cuda.get_device_properties(self.cuda_index).uuid)
+            return nv.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.cuda_index)
+
+    def _run(self, nv, h):
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            except Exception as exc:  # keep timing even if NVML hiccups
+                self.err = str(exc)
+            self._stop.wait(0.005)
 
     def __enter__(self):
+        import threading
+
         try:
-            self.path.parent.mkdir(exist_ok=True)
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=self.fh, stderr=subprocess.DEVNULL)
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._thread = threading.Thread(target=self._run, args=(nv, h), daemon=True)
+            self._thread.start()
+        except Exception as exc:
+            self.err = str(exc)
         return self
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
-            self.fh.close()
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join(timeout=2)
 
     def summary(self) -> dict:
-        if self.proc is None or not self.path.exists():
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.path.read_text().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        loaded = [s for s in sm if mx and s > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "error": self.err}
+        sm = [c for c, _ in self.samples]
+        loaded = [c for c in sm if self.max_mhz and c > 0.5 * self.max_mhz] or sm
+        reasons = sorted({name for _, r in self.samples for name, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "source": "NVML, 5 ms"}
 
 
 def dist_env():
@@ -155,7 +167,7 @@ def run_reference_arm(args) -> None:
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--quick", action="store_true", help="skip the side measurements")
@@ -257,6 +269,18 @@ def main() -> None:
                        "parallelism": f"counter/stream-range shards x{world}, no collective"},
             "roofline": roofline, "per_generator": per_gen, "gpu_launches": launches, "clocks": clocks}
 
+    # write-only HBM ceiling for context (cudaMemsetAsync over the same 4 GiB)
+    z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out.zero_()
+    z0.record(stream)
+    for _ in range(5):
+        out.zero_()
+    z1.record(stream)
+    z1.synchronize()
+    store_gbs = bytes_per_fill * 5 / (z0.elapsed_time(z1) / 1e3) / 1e9
+    roofline["store_only_gbs"] = round(store_gbs, 1)
+    roofline["frac_of_store_only"] = round(per_gen[dom]["hbm_gbs"] / store_gbs, 3)
+
     # ---------------- e2e through the public API, host buffers ----------------
     del out
     torch.cuda.empty_cache()
@@ -323,7 +347,7 @@ def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ran
     # ---- configs[2]: Brownian walk, 10M particles x 10k steps, pid-range shards ----
     n_part, n_steps = 10_000_000, 10_000
     lo, hi = rank * n_part, (rank + 1) * n_part  # weak scaling: each rank owns 10M pids
-    cfg = cb_cfg = brownian.SimConfig(n_part, n_steps)
+    cfg = brownian.SimConfig(n_part, n_steps)
     p = brownian.init_particles(cfg, pid_base=lo, n=hi - lo)
     x0 = [t.clone() for t in (p.x, p.y, p.vx, p.vy)]
 

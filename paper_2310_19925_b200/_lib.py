@@ -35,10 +35,10 @@ SIGNATURES = {
     "cbrng_version": (C.c_char_p, []),
     "cbrng_last_error": (C.c_char_p, []),
     "cbrng_device_sm_count": (i32, [i32]),
-    "cbrng_words": (i32, [i32, u64, u32, u32, vp, u64, vp, vp, vp]),
-    "cbrng_uniform_f32": (i32, [i32, u64, u32, u32, vp, u64, vp, vp, vp]),
-    "cbrng_uniform_f64": (i32, [i32, u64, u32, u32, vp, u64, vp, vp, vp]),
-    "cbrng_normal2_f64": (i32, [i32, u64, u32, u32, vp, u64, vp, vp, vp, vp]),
+    "cbrng_words": (i32, [i32, u64, u32, u64, vp, u64, vp, vp, vp]),
+    "cbrng_uniform_f32": (i32, [i32, u64, u32, u64, vp, u64, vp, vp, vp]),
+    "cbrng_uniform_f64": (i32, [i32, u64, u32, u64, vp, u64, vp, vp, vp]),
+    "cbrng_normal2_f64": (i32, [i32, u64, u32, u64, vp, u64, vp, vp, vp, vp]),
     "cbrng_tyche_fill": (i32, [vp, u64, vp, vp]),
     "cbrng_prefix_words": (i32, [i32, vp, u64, vp, u32, u64, u32, vp, vp]),
     "cbrng_prefix_uniform_f32": (i32, [i32, vp, u64, vp, u32, u64, u32, vp, vp]),

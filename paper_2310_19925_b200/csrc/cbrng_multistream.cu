@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(256) tyche_prefix_kernel(const __grid_constant
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t groups = a.nwords / 32, rem = a.nwords % 32;
+    const bool vec = (a.nwords % 4) == 0;
     for (uint64_t s0 = warp * 32; s0 < a.n_streams; s0 += nwarps * 32) {
         const uint64_t sid = s0 + lane;
         const bool valid = sid < a.n_streams;
@@ -153,7 +154,16 @@ __global__ void __launch_bounds__(256) tyche_prefix_kernel(const __grid_constant
 #pragma unroll
             for (int k = 0; k < 8; k++) {
                 const uint32_t r = k * 4 + (lane >> 3), c = lane & 7;
-                if (s0 + r < a.n_streams) store4<OUT>(a.out, (s0 + r) * a.nwords + g * 32 + c * 4, tile[wib][r][c]);
+                if (s0 + r < a.n_streams) {
+                    const uint64_t at = (s0 + r) * a.nwords + g * 32 + c * 4;
+                    const uint4 v = tile[wib][r][c];
+                    if (vec) {
+                        store4<OUT>(a.out, at, v);
+                    } else {  // rows not 16-byte aligned (nwords % 4 != 0)
+                        store1<OUT>(a.out, at, v.x); store1<OUT>(a.out, at + 1, v.y);
+                        store1<OUT>(a.out, at + 2, v.z); store1<OUT>(a.out, at + 3, v.w);
+                    }
+                }
             }
             __syncwarp();
         }
@@ -196,7 +206,7 @@ static int dispatch_prefix(int alg, const uint64_t *seeds, uint64_t seed_base, c
         case THREEFRY: return launch_prefix<THREEFRY, OUT>(a, st);
         case SQUARES: return launch_prefix<SQUARES, OUT>(a, st);
         default: {
-            if (nwords >= 32 && !aligned(out, 16)) {
+            if (nwords >= 32 && nwords % 4 == 0 && !aligned(out, 16)) {
                 set_error("output pointer not 16-byte aligned");
                 return CBRNG_EALIGN;
             }
