@@ -54,16 +54,8 @@ template <> struct Particle<THREEFRY> {
 template <> struct Particle<SQUARES> {
     uint64_t key;
     __device__ __forceinline__ explicit Particle(uint64_t pid) : key(squares_key(pid)) {}
-    __device__ __forceinline__ uint32_t w(uint64_t x) const {
-        uint64_t y = x, z = y + key;
-        x = swap32(x * x + y);
-        x = swap32(x * x + z);
-        x = swap32(x * x + y);
-        return (uint32_t)((x * x + z) >> 32);
-    }
     __device__ __forceinline__ uint4 words(uint32_t ctr) const {
-        uint64_t x0 = ((uint64_t)ctr << 32) * key;  // counter (ctr << 32) | k, k = 0..3
-        return make_uint4(w(x0), w(x0 + key), w(x0 + 2 * key), w(x0 + 3 * key));
+        return squares_x4(((uint64_t)ctr << 32) * key, key);  // counters (ctr << 32) | k, k = 0..3
     }
 };
 template <> struct Particle<TYCHE> {

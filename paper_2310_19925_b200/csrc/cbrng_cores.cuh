@@ -260,6 +260,52 @@ __host__ __device__ inline uint4 threefry_block_rounds(uint4 c, const uint32_t k
     return make_uint4(x[0], x[1], x[2], x[3]);
 }
 
+// Rotate-then-xor, two ways. SHF.L.W + LOP3 puts both ops on the ALU pipe;
+// IMAD.WIDE.U32 by 2^r yields (x << r, x >> (32-r)) in one FMA-heavy op and a
+// single LOP3 folds (lo | hi) ^ y. Threefry is ALU-bound (ncu: ALU 97 %, heavy
+// 40 %), so moving a share of its 40 rotations to the multiplier balances the
+// two pipes. The multiplier must be a runtime (parameter) value, or the
+// compiler turns the multiply back into shifts.
+template <bool MUL>
+__device__ __forceinline__ uint32_t rotx(uint32_t v, int r, uint32_t p2, uint32_t y) {
+    if constexpr (MUL) {
+        const uint64_t w = (uint64_t)v * p2;
+        return ((uint32_t)w | (uint32_t)(w >> 32)) ^ y;
+    } else {
+        return rotl32(v, r) ^ y;
+    }
+}
+
+// Spread NMUL multiplier-rotations evenly over the 40 rotations of a block.
+__host__ __device__ constexpr bool tf_mul(int rot, int nmul) { return nmul > 0 && ((rot * nmul) % 40) < nmul; }
+
+template <int R, int NMUL>
+__device__ __forceinline__ void threefry_round_m(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3,
+                                                 const uint32_t *p2) {
+    constexpr int ra = TfRot<R % 8>::a, rb = TfRot<R % 8>::b;
+    constexpr bool ma = tf_mul(2 * R, NMUL), mb = tf_mul(2 * R + 1, NMUL);
+    if (R % 2 == 0) {
+        x0 += x1; x1 = rotx<ma>(x1, ra, p2[2 * (R % 8)], x0);
+        x2 += x3; x3 = rotx<mb>(x3, rb, p2[2 * (R % 8) + 1], x2);
+    } else {
+        x0 += x3; x3 = rotx<ma>(x3, ra, p2[2 * (R % 8)], x0);
+        x2 += x1; x1 = rotx<mb>(x1, rb, p2[2 * (R % 8) + 1], x2);
+    }
+}
+
+template <int FIRST, int NMUL>
+__device__ __forceinline__ void threefry_rounds_m(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3,
+                                                  const uint32_t ks[5], const uint32_t *p2) {
+#define TF_RM(R)                                                                \
+    if (R >= FIRST) {                                                           \
+        threefry_round_m<R, NMUL>(x0, x1, x2, x3, p2);                          \
+        if ((R + 1) % 4 == 0) threefry_inject<(R + 1) / 4>(x0, x1, x2, x3, ks); \
+    }
+    TF_RM(0) TF_RM(1) TF_RM(2) TF_RM(3) TF_RM(4) TF_RM(5) TF_RM(6) TF_RM(7) TF_RM(8) TF_RM(9)
+    TF_RM(10) TF_RM(11) TF_RM(12) TF_RM(13) TF_RM(14) TF_RM(15) TF_RM(16) TF_RM(17) TF_RM(18) TF_RM(19)
+#undef TF_RM
+}
+
 // Single stream: key (k0, k1, sc, 0), ctr (bc, 0, 0, 0). Rounds 0-1 are mostly
 // launch-uniform; the host folds them.
 struct ThreefryStream {
@@ -269,6 +315,7 @@ struct ThreefryStream {
     uint32_t x2_0;  // ks2 + ks3 (round 0 x2)
     uint32_t x3_0;  // rotl(ks3, 26) ^ x2_0 (round 0 x3)
     uint32_t x3r;   // rotl(x3_0, 11) (round 1)
+    uint32_t p2[16];  // 2^R[r%8] multipliers for rotx<true>
 };
 
 inline ThreefryStream threefry_stream_setup(uint64_t seed, uint32_t sc) {
@@ -281,9 +328,12 @@ inline ThreefryStream threefry_stream_setup(uint64_t seed, uint32_t sc) {
     p.x2_0 = p.ks[2] + p.ks[3];
     p.x3_0 = rotl32(p.ks[3], 26) ^ p.x2_0;
     p.x3r = rotl32(p.x3_0, 11);
+    const int ROT[8][2] = {{10, 26}, {11, 21}, {13, 27}, {23, 5}, {6, 20}, {17, 11}, {25, 10}, {18, 20}};
+    for (int i = 0; i < 8; i++) { p.p2[2 * i] = 1u << ROT[i][0]; p.p2[2 * i + 1] = 1u << ROT[i][1]; }
     return p;
 }
 
+template <int NMUL = 0>
 __device__ __forceinline__ uint4 threefry_stream_block(const ThreefryStream& p, uint32_t bc) {
     // round 0 (even; rot 10, 26): x = (bc+ks0, ks1, ks2, ks3)
     uint32_t x0 = bc + p.s01;
@@ -294,7 +344,7 @@ __device__ __forceinline__ uint4 threefry_stream_block(const ThreefryStream& p, 
     uint32_t x3 = p.x3r ^ x0;
     uint32_t x2 = p.x2_0 + x1;
     x1 = rotl32(x1, 21) ^ x2;
-    threefry_rounds_from<2>(x0, x1, x2, x3, p.ks);
+    threefry_rounds_m<2, NMUL>(x0, x1, x2, x3, p.ks, p.p2);
     return make_uint4(x0, x1, x2, x3);
 }
 
@@ -320,10 +370,51 @@ __host__ __device__ __forceinline__ uint32_t squares_round(uint64_t key, uint64_
     return (uint32_t)((x * x + z) >> 32);
 }
 
+// One squaring step on 32-bit halves: (h, l) <- swap32((h:l)^2 + a) mod 2^64.
+// (h:l)^2 mod 2^64 = l*l + ((2*h*l) << 32): one IMAD.WIDE.U32 with the 64-bit
+// addend folded in, plus one IMAD for the cross term (h+h on the ALU pipe). The
+// generic 64-bit product costs IMAD.WIDE + 2 IMAD on the FMA-heavy pipe.
+__device__ __forceinline__ void squares_sq_swap(uint32_t &h, uint32_t &l, uint64_t a) {
+    const uint64_t p = (uint64_t)l * l + a;
+    const uint32_t hi = (uint32_t)(p >> 32) + l * (h + h);
+    h = (uint32_t)p;  // swap32: the low half becomes the high half
+    l = hi;
+}
+
+// squares32 from x = ctr*key (generators.py:173-187) on 32-bit halves.
+__device__ __forceinline__ uint32_t squares_from_x(uint64_t x, uint64_t key) {
+    const uint64_t y = x, z = x + key;
+    uint32_t h = (uint32_t)(x >> 32), l = (uint32_t)x;
+    squares_sq_swap(h, l, y);
+    squares_sq_swap(h, l, z);
+    squares_sq_swap(h, l, y);
+    // last round: only the high half of x*x + z
+    const uint64_t p = (uint64_t)l * l + z;
+    return (uint32_t)(p >> 32) + l * (h + h);
+}
+
+// Four consecutive counters c..c+3 of one key: x_{k+1} = x_k + key (64-bit add on
+// the ALU pipe) instead of another 64-bit multiply.
+__device__ __forceinline__ uint64_t add64_opaque(uint64_t a, uint64_t b) {
+    // add.cc/addc in inline PTX: the compiler cannot re-associate x0 + key back
+    // into (c+1)*key + base (which costs an IMAD.WIDE + IMAD on the FMA-heavy pipe).
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
+        : "=r"(lo), "=r"(hi)
+        : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)));
+    return ((uint64_t)hi << 32) | lo;
+}
+
+__device__ __forceinline__ uint4 squares_x4(uint64_t x0, uint64_t key) {
+    const uint64_t x1 = add64_opaque(x0, key), x2 = add64_opaque(x1, key), x3 = add64_opaque(x2, key);
+    return make_uint4(squares_from_x(x0, key), squares_from_x(x1, key), squares_from_x(x2, key),
+                      squares_from_x(x3, key));
+}
+
 // Single stream: ctr = (sc << 32) | bc, so ctr*key = bc*key + ((sc*key_lo) << 32).
 struct SquaresStream {
     uint64_t key;
-    uint64_t base;  // (sc*key) mod 2^64 restricted to the sc<<32 term: (sc*key_lo) << 32
+    uint64_t base;  // (sc << 32) * key mod 2^64
 };
 
 inline SquaresStream squares_stream_setup(uint64_t seed, uint32_t sc) {
@@ -333,12 +424,18 @@ inline SquaresStream squares_stream_setup(uint64_t seed, uint32_t sc) {
     return p;
 }
 
-__device__ __forceinline__ uint32_t squares_stream_word(const SquaresStream& p, uint32_t bc) {
-    uint64_t x = (uint64_t)bc * p.key + p.base, y = x, z = y + p.key;
-    x = swap32(x * x + y);
-    x = swap32(x * x + z);
-    x = swap32(x * x + y);
-    return (uint32_t)((x * x + z) >> 32);
+__device__ __forceinline__ uint32_t squares_stream_word(const SquaresStream &p, uint32_t bc) {
+    return squares_from_x((uint64_t)bc * p.key + p.base, p.key);
+}
+
+// Words bc..bc+3 (counters wrap mod 2^32 in the low half only, bulk.py:268): the
+// incremental form is exact unless bc+k wraps, which the caller checks.
+__device__ __forceinline__ uint4 squares_stream_word4(const SquaresStream &p, uint32_t bc) {
+    if (bc > 0xFFFFFFFCu) {
+        return make_uint4(squares_stream_word(p, bc), squares_stream_word(p, bc + 1), squares_stream_word(p, bc + 2),
+                          squares_stream_word(p, bc + 3));
+    }
+    return squares_x4((uint64_t)bc * p.key + p.base, p.key);
 }
 
 // ---------------------------------------------------------------------------

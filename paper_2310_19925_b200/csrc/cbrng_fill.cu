@@ -14,6 +14,8 @@
 // 4 - skip words of block b0 + u followed by the first skip words of block
 // b0 + u + 1 (a resumed, mid-block generator: 2 cipher calls per unit).
 // Squares word k of unit u uses counter (word_pos + 4u + k) mod 2^32 (bulk.py:268).
+#include <cstdlib>
+
 #include "cbrng_internal.cuh"
 
 namespace cbrng {
@@ -36,22 +38,22 @@ struct FillArgs {
     void *out1;
 };
 
-template <int ALG>
+// V selects a code variant per algorithm; for Threefry it is the number of
+// rotations done on the multiplier (rotx<true>): V = 0, 1, 2 -> 0, 12, 20 of 40.
+template <int ALG, int V>
 __device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, uint32_t bc) {
     if constexpr (ALG == PHILOX) return philox_stream_block(p, bc);
-    else return threefry_stream_block(p, bc);
+    else return threefry_stream_block<V == 0 ? 0 : (V == 1 ? 12 : 20)>(p, bc);
 }
 
-template <int ALG, bool SKIP>
+template <int ALG, bool SKIP, int V = 0>
 __device__ __forceinline__ uint4 unit_words(const typename StreamOf<ALG>::T &p, uint32_t bc0, uint32_t skip, uint64_t u) {
     if constexpr (ALG == SQUARES) {
-        uint32_t c = bc0 + 4u * (uint32_t)u;
-        return make_uint4(squares_stream_word(p, c), squares_stream_word(p, c + 1),
-                          squares_stream_word(p, c + 2), squares_stream_word(p, c + 3));
+        return squares_stream_word4(p, bc0 + 4u * (uint32_t)u);
     } else if constexpr (!SKIP) {
-        return block_at<ALG>(p, bc0 + (uint32_t)u);
+        return block_at<ALG, V>(p, bc0 + (uint32_t)u);
     } else {
-        uint4 a = block_at<ALG>(p, bc0 + (uint32_t)u), b = block_at<ALG>(p, bc0 + (uint32_t)u + 1);
+        uint4 a = block_at<ALG, V>(p, bc0 + (uint32_t)u), b = block_at<ALG, V>(p, bc0 + (uint32_t)u + 1);
         if (skip == 1) return make_uint4(a.y, a.z, a.w, b.x);
         if (skip == 2) return make_uint4(a.z, a.w, b.x, b.y);
         return make_uint4(a.w, b.x, b.y, b.z);
@@ -88,24 +90,29 @@ __device__ __forceinline__ void store_tail(void *out0, uint64_t u, uint32_t tail
     }
 }
 
-template <int ALG, int OUT, int ILP, bool SKIP>
+template <int ALG, int OUT, int ILP, bool SKIP, int V>
 __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     constexpr uint32_t TILE = 32 * ILP;
-    for (uint64_t base = warp * TILE; base < a.n_units; base += nwarps * TILE) {
+    // Full warp tiles: no bounds checks, all ILP cipher evaluations issued
+    // before the stores.
+    const uint64_t n_full = a.n_units / TILE;
+    for (uint64_t t = warp; t < n_full; t += nwarps) {
+        const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
 #pragma unroll
-        for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP>(a.p, a.bc0, a.skip, base + lane + 32 * j);
+        for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, base + 32 * j);
 #pragma unroll
-        for (int j = 0; j < ILP; j++) {
-            uint64_t u = base + lane + 32 * j;
-            if (u < a.n_units) store_unit<OUT>(a.out0, a.out1, u, w[j]);
-        }
+        for (int j = 0; j < ILP; j++) store_unit<OUT>(a.out0, a.out1, base + 32 * j, w[j]);
     }
-    if (a.tail && blockIdx.x == 0 && threadIdx.x == 0) {
-        store_tail<OUT>(a.out0, a.n_units, a.tail, unit_words<ALG, SKIP>(a.p, a.bc0, a.skip, a.n_units));
+    // Remainder (< one tile) and the partial trailing unit: the last warp of the grid.
+    if (warp == nwarps - 1) {
+        for (uint64_t u = n_full * TILE + lane; u < a.n_units; u += 32)
+            store_unit<OUT>(a.out0, a.out1, u, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, u));
+        if (a.tail && lane == 0)
+            store_tail<OUT>(a.out0, a.n_units, a.tail, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, a.n_units));
     }
 }
 
@@ -145,14 +152,56 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
 
 constexpr int FILL_BLOCK = 256;
 
-template <int ALG, int OUT, bool SKIP>
-static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
-    constexpr int ILP = 2;
-    auto k = fill_kernel<ALG, OUT, ILP, SKIP>;
+template <int ALG, int OUT, bool SKIP, int ILP, int V>
+static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
+    auto k = fill_kernel<ALG, OUT, ILP, SKIP, V>;
     uint64_t work = (a.n_units + (FILL_BLOCK * ILP) - 1) / (FILL_BLOCK * ILP);
     unsigned grid = grid_for(k, FILL_BLOCK, 0, work ? work : 1);
     k<<<grid, FILL_BLOCK, 0, st>>>(a);
     return check_launch("fill_kernel");
+}
+
+// Units per thread per tile. Default 2 (two independent cipher chains in
+// flight per thread on top of full occupancy); CBRNG_FILL_ILP=1|2|4 overrides
+// for tuning runs.
+static int fill_ilp() {
+    static int v = [] {
+        const char *e = getenv("CBRNG_FILL_ILP");
+        int x = e ? atoi(e) : 2;
+        return (x == 1 || x == 2 || x == 4) ? x : 2;
+    }();
+    return v;
+}
+
+// Threefry rotation split (see rotx in cbrng_cores.cuh); CBRNG_TF_VARIANT=0|1|2.
+static int tf_variant() {
+    static int v = [] {
+        const char *e = getenv("CBRNG_TF_VARIANT");
+        int x = e ? atoi(e) : 0;
+        return (x >= 0 && x <= 2) ? x : 0;
+    }();
+    return v;
+}
+
+template <int ALG, int OUT, bool SKIP, int V>
+static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
+    switch (fill_ilp()) {
+        case 1: return launch_fill_ilp<ALG, OUT, SKIP, 1, V>(a, st);
+        case 4: return launch_fill_ilp<ALG, OUT, SKIP, 4, V>(a, st);
+        default: return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);
+    }
+}
+
+template <int ALG, int OUT, bool SKIP>
+static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
+    if constexpr (ALG == THREEFRY) {
+        switch (tf_variant()) {
+            case 1: return launch_fill_v<ALG, OUT, SKIP, 1>(a, st);
+            case 2: return launch_fill_v<ALG, OUT, SKIP, 2>(a, st);
+            default: break;
+        }
+    }
+    return launch_fill_v<ALG, OUT, SKIP, 0>(a, st);
 }
 
 template <int ALG, int OUT>

@@ -46,22 +46,13 @@ template <> struct StreamKey<THREEFRY> {
     __device__ __forceinline__ uint4 block(uint32_t b) const { return threefry_block(make_uint4(b, 0, 0, 0), k0, k1, sc, 0); }
 };
 template <> struct StreamKey<SQUARES> {
-    uint64_t key, base;
+    SquaresStream p;
     __device__ __forceinline__ StreamKey(uint64_t seed, uint32_t c) {
-        key = squares_key(seed);
-        base = ((uint64_t)c << 32) * key;
+        p.key = squares_key(seed);
+        p.base = ((uint64_t)c << 32) * p.key;
     }
-    __device__ __forceinline__ uint32_t word(uint32_t j) const {
-        uint64_t x = (uint64_t)j * key + base, y = x, z = y + key;
-        x = swap32(x * x + y);
-        x = swap32(x * x + z);
-        x = swap32(x * x + y);
-        return (uint32_t)((x * x + z) >> 32);
-    }
-    __device__ __forceinline__ uint4 block(uint32_t b) const {
-        uint32_t j = 4 * b;
-        return make_uint4(word(j), word(j + 1), word(j + 2), word(j + 3));
-    }
+    __device__ __forceinline__ uint32_t word(uint32_t j) const { return squares_stream_word(p, j); }
+    __device__ __forceinline__ uint4 block(uint32_t b) const { return squares_stream_word4(p, 4 * b); }
 };
 
 template <int ALG>
@@ -125,15 +116,20 @@ __global__ void __launch_bounds__(256) prefix_kernel(const __grid_constant__ Pre
 }
 
 constexpr int TY_WARPS = 8;  // 256 threads
-constexpr int TY_PAD = 9;    // 8 x 16-byte chunks + 1 pad = 144-byte rows: conflict-free STS.128/LDS.128
+constexpr int TY_CH = 4;     // staged 16-byte chunks per stream row = 16 words (64 B)
+
+// Staging slot of (row r, chunk c) in a warp's 32 x 4-chunk tile. The XOR
+// swizzle keeps both the row-wise STS.128 (lane = row) and the column-wise
+// LDS.128 (8 lanes = 2 rows x 4 chunks) conflict-free, without padding.
+__device__ __forceinline__ uint32_t ty_slot(uint32_t r, uint32_t c) { return r * TY_CH + (c ^ ((r >> 1) & 3)); }
 
 template <int OUT>
-__global__ void __launch_bounds__(256) tyche_prefix_kernel(const __grid_constant__ PrefixArgs a) {
-    __shared__ uint4 tile[TY_WARPS][32][TY_PAD];
+__global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_constant__ PrefixArgs a) {
+    __shared__ uint4 tile[TY_WARPS][32 * TY_CH];  // 16 KB per CTA: 8 CTAs (64 warps) fit an SM
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t groups = a.nwords / 32, rem = a.nwords % 32;
+    const uint32_t groups = a.nwords / 16, rem = a.nwords % 16;
     const bool vec = (a.nwords % 4) == 0;
     for (uint64_t s0 = warp * 32; s0 < a.n_streams; s0 += nwarps * 32) {
         const uint64_t sid = s0 + lane;
@@ -142,21 +138,21 @@ __global__ void __launch_bounds__(256) tyche_prefix_kernel(const __grid_constant
         uint32_t A = st.x, B = st.y, C = st.z, D = st.w;
         for (uint32_t g = 0; g < groups; g++) {
 #pragma unroll
-            for (int c = 0; c < 8; c++) {
+            for (int c = 0; c < TY_CH; c++) {
                 uint4 w;
                 tyche_mix(A, B, C, D); w.x = B;
                 tyche_mix(A, B, C, D); w.y = B;
                 tyche_mix(A, B, C, D); w.z = B;
                 tyche_mix(A, B, C, D); w.w = B;
-                tile[wib][lane][c] = w;
+                tile[wib][ty_slot(lane, c)] = w;
             }
             __syncwarp();
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                const uint32_t r = k * 4 + (lane >> 3), c = lane & 7;
+            for (int k = 0; k < 4; k++) {
+                const uint32_t r = k * 8 + (lane >> 2), c = lane & 3;
                 if (s0 + r < a.n_streams) {
-                    const uint64_t at = (s0 + r) * a.nwords + g * 32 + c * 4;
-                    const uint4 v = tile[wib][r][c];
+                    const uint64_t at = (s0 + r) * a.nwords + g * 16 + c * 4;
+                    const uint4 v = tile[wib][ty_slot(r, c)];
                     if (vec) {
                         store4<OUT>(a.out, at, v);
                     } else {  // rows not 16-byte aligned (nwords % 4 != 0)
@@ -169,7 +165,7 @@ __global__ void __launch_bounds__(256) tyche_prefix_kernel(const __grid_constant
         }
         for (uint32_t j = 0; j < rem; j++) {
             tyche_mix(A, B, C, D);
-            if (valid) store1<OUT>(a.out, sid * a.nwords + groups * 32 + j, B);
+            if (valid) store1<OUT>(a.out, sid * a.nwords + groups * 16 + j, B);
         }
     }
 }
@@ -206,7 +202,7 @@ static int dispatch_prefix(int alg, const uint64_t *seeds, uint64_t seed_base, c
         case THREEFRY: return launch_prefix<THREEFRY, OUT>(a, st);
         case SQUARES: return launch_prefix<SQUARES, OUT>(a, st);
         default: {
-            if (nwords >= 32 && nwords % 4 == 0 && !aligned(out, 16)) {
+            if (nwords >= 16 && nwords % 4 == 0 && !aligned(out, 16)) {
                 set_error("output pointer not 16-byte aligned");
                 return CBRNG_EALIGN;
             }

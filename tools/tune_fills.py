@@ -1,0 +1,49 @@
+"""Time the configs[1] fills under code variants (env knobs read once per process).
+
+    python tools/tune_fills.py            # sweeps CBRNG_FILL_ILP x CBRNG_TF_VARIANT
+"""
+import itertools
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+
+CHILD = r'''
+import sys, json, torch
+sys.path.insert(0, %r)
+from paper_2310_19925_b200 import _lib
+L = _lib.lib(); s = int(torch.cuda.current_stream().cuda_stream)
+N = 1 << 30
+out = torch.empty(N, dtype=torch.float32, device="cuda")
+res = {}
+def run(name, fn, reps=20):
+    fn(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps): fn()
+    e1.record(); e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    res[name] = {"ms": round(ms, 4), "gbs": round(N * 4 / ms / 1e6, 1)}
+for a, nm in enumerate(["philox", "threefry", "squares"]):
+    run(nm, lambda a=a: _lib.check(L.cbrng_uniform_f32(a, 42, 0, 0, None, N, out.data_ptr(), None, s)))
+run("tyche_ms", lambda: _lib.check(L.cbrng_prefix_uniform_f32(3, None, 0, None, 0, 1 << 22, 256, out.data_ptr(), s)))
+run("philox_ms_u32", lambda: _lib.check(L.cbrng_prefix_words(0, None, 0, None, 0, 1 << 22, 256, out.data_ptr(), s)))
+run("memset", lambda: out.zero_())
+print(json.dumps(res))
+'''
+
+rows = []
+for ilp, tfv in itertools.product([1, 2, 4], [0, 1, 2]):
+    env = dict(os.environ, CBRNG_FILL_ILP=str(ilp), CBRNG_TF_VARIANT=str(tfv))
+    r = subprocess.run([sys.executable, "-c", CHILD % str(ROOT)], env=env, capture_output=True, text=True)
+    if r.returncode:
+        print(r.stderr[-2000:])
+        continue
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    rows.append((ilp, tfv, d))
+    print(f"ILP={ilp} TF={tfv} " + " ".join(f"{k}={v['gbs']}" for k, v in d.items()), flush=True)
+Path(ROOT / "gpurun_out").mkdir(exist_ok=True)
+(ROOT / "gpurun_out" / "tune_fills.json").write_text(json.dumps(rows, indent=1))
