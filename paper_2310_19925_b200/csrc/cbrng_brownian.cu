@@ -18,6 +18,8 @@
 // FP64 arithmetic is bit-exact with numpy's evaluation order:
 //   vx -= ((gamma/mass) * vx) * dt;  vx += (r * 2.0 - 1.0) * sqrt(dt);  x += vx * dt
 // with every operation an explicit round-to-nearest intrinsic (no FMA contraction).
+#include <cmath>
+
 #include "cbrng_internal.cuh"
 
 namespace cbrng {
@@ -31,34 +33,36 @@ struct BrownArgs {
     uint64_t first_it;
     uint64_t nsteps;
     double gm, dt, sqrt_dt;
+    double kick_scale;  // sqrt_dt * 2^-52 (see kick())
+    int fold;           // kick_scale is exact and normal: use the folded kick
 };
 
 // Per-particle, step-invariant state.
-template <int ALG> struct Particle;
-template <> struct Particle<PHILOX> {
-    PhiloxParticle p;
-    __device__ __forceinline__ explicit Particle(uint64_t pid) : p(philox_particle_setup(pid)) {}
+template <int ALG, bool HI0 = false> struct Particle;
+template <bool HI0> struct Particle<PHILOX, HI0> {
+    PhiloxParticle<HI0> p;
+    __device__ __forceinline__ explicit Particle(uint64_t pid) : p(philox_particle_setup<HI0>(pid)) {}
     __device__ __forceinline__ uint4 words(uint32_t ctr) const {
         uint32_t mh, ml;
         mulhilo(PHILOX_M0, ctr, mh, ml);
-        return philox_particle_block(p, mh, ml);
+        return philox_particle_block<HI0>(p, mh, ml);
     }
 };
-template <> struct Particle<THREEFRY> {
+template <bool HI0> struct Particle<THREEFRY, HI0> {
     uint32_t k0, k1;
     __device__ __forceinline__ explicit Particle(uint64_t pid) : k0((uint32_t)pid), k1((uint32_t)(pid >> 32)) {}
     __device__ __forceinline__ uint4 words(uint32_t ctr) const {
         return threefry_block(make_uint4(0, 0, 0, 0), k0, k1, ctr, 0);
     }
 };
-template <> struct Particle<SQUARES> {
+template <bool HI0> struct Particle<SQUARES, HI0> {
     uint64_t key;
     __device__ __forceinline__ explicit Particle(uint64_t pid) : key(squares_key(pid)) {}
     __device__ __forceinline__ uint4 words(uint32_t ctr) const {
         return squares_x4(((uint64_t)ctr << 32) * key, key);  // counters (ctr << 32) | k, k = 0..3
     }
 };
-template <> struct Particle<TYCHE> {
+template <bool HI0> struct Particle<TYCHE, HI0> {
     uint64_t pid;
     __device__ __forceinline__ explicit Particle(uint64_t p) : pid(p) {}
     __device__ __forceinline__ uint4 words(uint32_t ctr) const {
@@ -115,29 +119,43 @@ __global__ void __launch_bounds__(256) brownian_init_kernel(const __grid_constan
     }
 }
 
-// One dynamics step of one particle (brownian.py:129-142).
-__device__ __forceinline__ void step_update(double &x, double &y, double &vx, double &vy, uint4 w, double gm, double dt,
-                                            double sqrt_dt) {
-    vx = __dsub_rn(vx, __dmul_rn(__dmul_rn(gm, vx), dt));
-    vy = __dsub_rn(vy, __dmul_rn(__dmul_rn(gm, vy), dt));
-    const double rx = u32x2_to_f64(w.x, w.y);
-    const double ry = u32x2_to_f64(w.z, w.w);
-    vx = __dadd_rn(vx, __dmul_rn(__dsub_rn(__dmul_rn(rx, 2.0), 1.0), sqrt_dt));
-    vy = __dadd_rn(vy, __dmul_rn(__dsub_rn(__dmul_rn(ry, 2.0), 1.0), sqrt_dt));
-    x = __dadd_rn(x, __dmul_rn(vx, dt));
-    y = __dadd_rn(y, __dmul_rn(vy, dt));
+// The kick (r * 2.0 - 1.0) * sqrt(dt) of brownian.py:139-140 with r =
+// ((lo | hi << 32) >> 11) * 2^-53. r*2 and r*2-1 are exact, and r*2-1 =
+// v * 2^-52 with v = (u >> 11) - 2^52 = ((int64)(u ^ 2^63)) >> 11 (a signed
+// 53-bit integer, converted exactly). Scaling by a power of two commutes with
+// rounding (no subnormals here), so round((v * 2^-52) * s) == round(v * (s *
+// 2^-52)): one conversion + one DMUL instead of conversion + 3 DMUL/DADD +
+// DMUL, bit-identical (tests/test_gpu_parity.py::TestBrownian).
+template <bool FOLD>
+__device__ __forceinline__ double kick(uint32_t lo, uint32_t hi, double sqrt_dt, double kick_scale) {
+    if constexpr (FOLD) {
+        const int64_t v = (int64_t)(((uint64_t)(hi ^ 0x80000000u) << 32) | lo) >> 11;
+        return __dmul_rn(__ll2double_rn(v), kick_scale);
+    } else {
+        return __dmul_rn(__dsub_rn(__dmul_rn(u32x2_to_f64(lo, hi), 2.0), 1.0), sqrt_dt);
+    }
 }
 
-template <int ALG>
+// One dynamics step of one particle (brownian.py:129-142).
+template <bool FOLD>
+__device__ __forceinline__ void step_update(double &x, double &y, double &vx, double &vy, uint4 w, const BrownArgs &a) {
+    vx = __dsub_rn(vx, __dmul_rn(__dmul_rn(a.gm, vx), a.dt));
+    vy = __dsub_rn(vy, __dmul_rn(__dmul_rn(a.gm, vy), a.dt));
+    vx = __dadd_rn(vx, kick<FOLD>(w.x, w.y, a.sqrt_dt, a.kick_scale));
+    vy = __dadd_rn(vy, kick<FOLD>(w.z, w.w, a.sqrt_dt, a.kick_scale));
+    x = __dadd_rn(x, __dmul_rn(vx, a.dt));
+    y = __dadd_rn(y, __dmul_rn(vy, a.dt));
+}
+
+template <int ALG, bool HI0, bool FOLD>
 __global__ void __launch_bounds__(256) brownian_steps_kernel(const __grid_constant__ BrownArgs a) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t pid = a.pid ? a.pid[i] : a.pid_base + i;
         double x = a.x[i], y = a.y[i], vx = a.vx[i], vy = a.vy[i];
-        const Particle<ALG> P(pid);
+        const Particle<ALG, HI0> P(pid);
         uint32_t ctr = a.init_ctr + (uint32_t)a.first_it;
-        for (uint64_t s = 0; s < a.nsteps; s++, ctr++) {
-            step_update(x, y, vx, vy, P.words(ctr), a.gm, a.dt, a.sqrt_dt);
-        }
+        const uint32_t nsteps = (uint32_t)a.nsteps;  // host splits launches at 2^32 - 1 steps
+        for (uint32_t s = 0; s < nsteps; s++, ctr++) step_update<FOLD>(x, y, vx, vy, P.words(ctr), a);
         a.x[i] = x; a.y[i] = y; a.vx[i] = vx; a.vy[i] = vy;
     }
 }
@@ -197,23 +215,33 @@ __global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint
     }
 }
 
-template <int ALG>
-static int launch_steps(BrownArgs a, int mode, cudaStream_t st) {
-    auto k = brownian_steps_kernel<ALG>;
+template <int ALG, bool HI0, bool FOLD>
+static int launch_steps_k(BrownArgs a, int mode, cudaStream_t st) {
+    auto k = brownian_steps_kernel<ALG, HI0, FOLD>;
     // One thread per particle: the fused kernel needs every particle resident
     // or queued, so the grid covers n (no persistence).
     const unsigned grid = (unsigned)((a.n + 255) / 256);
-    if (mode == CBRNG_BROWNIAN_FUSED) {
-        k<<<grid, 256, 0, st>>>(a);
-        return check_launch("brownian_steps_kernel");
-    }
     const uint64_t total = a.nsteps;
-    a.nsteps = 1;
-    for (uint64_t s = 0; s < total; s++) {
+    const uint64_t per_launch = mode == CBRNG_BROWNIAN_FUSED ? 0xFFFFFFFFull : 1;
+    for (uint64_t done = 0; done < total;) {
+        a.nsteps = total - done < per_launch ? total - done : per_launch;
         k<<<grid, 256, 0, st>>>(a);
-        a.first_it += 1;
+        a.first_it += a.nsteps;
+        done += a.nsteps;
     }
     return check_launch("brownian_steps_kernel");
+}
+
+template <int ALG>
+static int launch_steps(BrownArgs a, int mode, cudaStream_t st) {
+    // pid < 2^32 everywhere (implicit pids): the high key word is zero.
+    const bool hi0 = a.pid == nullptr && a.pid_base + a.n <= (1ull << 32);
+    if (a.fold) {
+        if (hi0) return launch_steps_k<ALG, true, true>(a, mode, st);
+        return launch_steps_k<ALG, false, true>(a, mode, st);
+    }
+    if (hi0) return launch_steps_k<ALG, true, false>(a, mode, st);
+    return launch_steps_k<ALG, false, false>(a, mode, st);
 }
 
 }  // namespace cbrng
@@ -228,7 +256,7 @@ int cbrng_brownian_init(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_b
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(x && y && vx && vy, "NULL particle array");
-    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, 0, 0, 0.0, 0.0, 0.0};
+    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, 0, 0, 0.0, 0.0, 0.0, 0.0, 0};
     cudaStream_t st = as_stream(stream);
     const unsigned grid = (unsigned)((n + 255) / 256);
     switch (alg) {
@@ -251,7 +279,10 @@ int cbrng_brownian_steps(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_
     if (n == 0 || nsteps == 0) return CBRNG_OK;
     CBRNG_REQUIRE(x && y && vx && vy, "NULL particle array");
     // Host-side scalars exactly as the reference forms them (brownian.py:134, :177).
-    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, first_it, nsteps, gamma / mass, dt, std::sqrt(dt)};
+    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, first_it, nsteps, gamma / mass, dt, std::sqrt(dt), 0.0, 0};
+    a.kick_scale = a.sqrt_dt * 0x1p-52;
+    // fold only when the scaled constant is exact (normal, no underflow)
+    a.fold = a.sqrt_dt == 0.0 || (a.kick_scale >= 0x1p-1022 && a.kick_scale * 0x1p52 == a.sqrt_dt);
     cudaStream_t st = as_stream(stream);
     switch (alg) {
         case PHILOX: return launch_steps<PHILOX>(a, mode, st);

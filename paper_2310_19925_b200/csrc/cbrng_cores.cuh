@@ -35,7 +35,13 @@ __host__ __device__ __forceinline__ uint32_t rotl32(uint32_t x, int r) {
 }
 
 __host__ __device__ __forceinline__ void mulhilo(uint32_t a, uint32_t b, uint32_t& hi, uint32_t& lo) {
-    uint64_t p = (uint64_t)a * b;  // IMAD.WIDE.U32
+#ifdef __CUDA_ARCH__
+    // mul.wide.u32 -> IMAD.WIDE.U32 (one FMA-heavy op for both halves)
+    uint64_t p;
+    asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+#else
+    uint64_t p = (uint64_t)a * b;
+#endif
     hi = (uint32_t)(p >> 32);
     lo = (uint32_t)p;
 }
@@ -135,40 +141,61 @@ __device__ __forceinline__ uint4 philox_stream_block(const PhiloxStream& p, uint
 }
 
 // Per-particle Philox for the Brownian walk: key = pid, ctr = (counter, 0, 0, 0).
-// Everything that depends only on pid is hoisted out of the step loop.
+// Everything that depends only on pid is hoisted out of the step loop. HI0:
+// every pid < 2^32 (the reference's np.arange pids for n <= 2^32), so the
+// high key word is 0 and its round keys K1[r] = r*W1 are compile-time
+// constants — 10 fewer registers per particle.
+template <bool HI0>
 struct PhiloxParticle {
-    uint32_t k0[10], k1[10];
+    uint32_t k0[10], k1[HI0 ? 1 : 10];
     uint32_t q1;       // round 1: c2 = c3 ^ q1, q1 = hi(M0*pid_lo) ^ K1[1]
-    uint32_t p0lo;     // round 1: c3 = lo(M0*pid_lo)
-    uint32_t r2;       // round 2: c2 = hi(M0*c0) ^ r2, r2 = p0lo ^ K1[2]
+    uint32_t r2;       // round 2: c2 = hi(M0*c0) ^ r2, r2 = lo(M0*pid_lo) ^ K1[2]
+    __device__ __forceinline__ uint32_t K1(int r) const {
+        if constexpr (HI0) return (uint32_t)r * PHILOX_W1;
+        else return k1[r];
+    }
 };
 
-__device__ __forceinline__ PhiloxParticle philox_particle_setup(uint64_t pid) {
-    PhiloxParticle p;
+template <bool HI0>
+__device__ __forceinline__ PhiloxParticle<HI0> philox_particle_setup(uint64_t pid) {
+    PhiloxParticle<HI0> p;
     p.k0[0] = (uint32_t)pid;
-    p.k1[0] = (uint32_t)(pid >> 32);
 #pragma unroll
-    for (int r = 1; r < 10; r++) { p.k0[r] = p.k0[r - 1] + PHILOX_W0; p.k1[r] = p.k1[r - 1] + PHILOX_W1; }
+    for (int r = 1; r < 10; r++) p.k0[r] = p.k0[r - 1] + PHILOX_W0;
+    if constexpr (!HI0) {
+        p.k1[0] = (uint32_t)(pid >> 32);
+#pragma unroll
+        for (int r = 1; r < 10; r++) p.k1[r] = p.k1[r - 1] + PHILOX_W1;
+    }
     uint32_t h, l;
     mulhilo(PHILOX_M0, p.k0[0], h, l);
-    p.q1 = h ^ p.k1[1];
-    p.p0lo = l;
-    p.r2 = l ^ p.k1[2];
+    p.q1 = h ^ p.K1(1);
+    p.r2 = l ^ p.K1(2);
+    // Pin the round keys in registers: without this the compiler re-derives
+    // k[r] = k[0] + r*W inside the step loop (18 VIADDs per step on the
+    // FMA-heavy pipe, ncu r1a) to save registers.
+#pragma unroll
+    for (int r = 0; r < 10; r++) asm volatile("" : "+r"(p.k0[r]));
+    if constexpr (!HI0) {
+#pragma unroll
+        for (int r = 0; r < 10; r++) asm volatile("" : "+r"(p.k1[r]));
+    }
     return p;
 }
 
 // Block 0 of stream (pid, ctr); mh/ml = hi/lo(M0*ctr) are step-uniform.
-__device__ __forceinline__ uint4 philox_particle_block(const PhiloxParticle& p, uint32_t mh, uint32_t ml) {
+template <bool HI0>
+__device__ __forceinline__ uint4 philox_particle_block(const PhiloxParticle<HI0>& p, uint32_t mh, uint32_t ml) {
     uint32_t c0, c1, c2, c3, h, l;
-    // round 0: c = (ctr, 0, 0, 0): c0 = 0 ^ 0 ^ K0 = pid_lo ; c1 = 0 ; c2 = hi(M0*ctr) ^ K1 ; c3 = lo(M0*ctr)
-    c2 = mh ^ p.k1[0];
+    // round 0: c = (ctr, 0, 0, 0): c0 = pid_lo ; c1 = 0 ; c2 = hi(M0*ctr) ^ K1 ; c3 = lo(M0*ctr)
+    c2 = mh ^ p.K1(0);
     c3 = ml;
     // round 1: p0 = M0*pid_lo (hoisted), p1 = M1*c2
     mulhilo(PHILOX_M1, c2, h, l);
     c0 = h ^ p.k0[1];  // c1 == 0
     c1 = l;
     c2 = c3 ^ p.q1;
-    // round 2: c3 == p0lo (hoisted) is folded into r2
+    // round 2: c3 == lo(M0*pid_lo) (hoisted) is folded into r2
     {
         uint32_t h0, l0, h1, l1;
         mulhilo(PHILOX_M0, c0, h0, l0);
@@ -179,7 +206,7 @@ __device__ __forceinline__ uint4 philox_particle_block(const PhiloxParticle& p, 
         c3 = l0;
     }
 #pragma unroll
-    for (int r = 3; r < 10; r++) philox_round(c0, c1, c2, c3, p.k0[r], p.k1[r]);
+    for (int r = 3; r < 10; r++) philox_round(c0, c1, c2, c3, p.k0[r], p.K1(r));
     return make_uint4(c0, c1, c2, c3);
 }
 
@@ -279,26 +306,39 @@ __device__ __forceinline__ uint32_t rotx(uint32_t v, int r, uint32_t p2, uint32_
 // Spread NMUL multiplier-rotations evenly over the 40 rotations of a block.
 __host__ __device__ constexpr bool tf_mul(int rot, int nmul) { return nmul > 0 && ((rot * nmul) % 40) < nmul; }
 
-template <int R, int NMUL>
-__device__ __forceinline__ void threefry_round_m(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3,
-                                                 const uint32_t *p2) {
-    constexpr int ra = TfRot<R % 8>::a, rb = TfRot<R % 8>::b;
-    constexpr bool ma = tf_mul(2 * R, NMUL), mb = tf_mul(2 * R + 1, NMUL);
-    if (R % 2 == 0) {
-        x0 += x1; x1 = rotx<ma>(x1, ra, p2[2 * (R % 8)], x0);
-        x2 += x3; x3 = rotx<mb>(x3, rb, p2[2 * (R % 8) + 1], x2);
+// a + b forced onto the FMA-heavy pipe: mad.lo with a multiplier the compiler
+// cannot see is 1 (a kernel parameter), so ptxas must emit IMAD, not IADD3.
+template <bool FORCE>
+__device__ __forceinline__ uint32_t addp(uint32_t a, uint32_t b, uint32_t one) {
+    if constexpr (FORCE) {
+        uint32_t r;
+        asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(one), "r"(a));
+        return r;
     } else {
-        x0 += x3; x3 = rotx<ma>(x3, ra, p2[2 * (R % 8)], x0);
-        x2 += x1; x1 = rotx<mb>(x1, rb, p2[2 * (R % 8) + 1], x2);
+        return a + b;
     }
 }
 
-template <int FIRST, int NMUL>
+template <int R, int NMUL, bool ADDMUL>
+__device__ __forceinline__ void threefry_round_m(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3,
+                                                 const uint32_t *p2, uint32_t one) {
+    constexpr int ra = TfRot<R % 8>::a, rb = TfRot<R % 8>::b;
+    constexpr bool ma = tf_mul(2 * R, NMUL), mb = tf_mul(2 * R + 1, NMUL);
+    if (R % 2 == 0) {
+        x0 = addp<ADDMUL>(x0, x1, one); x1 = rotx<ma>(x1, ra, p2[2 * (R % 8)], x0);
+        x2 = addp<ADDMUL>(x2, x3, one); x3 = rotx<mb>(x3, rb, p2[2 * (R % 8) + 1], x2);
+    } else {
+        x0 = addp<ADDMUL>(x0, x3, one); x3 = rotx<ma>(x3, ra, p2[2 * (R % 8)], x0);
+        x2 = addp<ADDMUL>(x2, x1, one); x1 = rotx<mb>(x1, rb, p2[2 * (R % 8) + 1], x2);
+    }
+}
+
+template <int FIRST, int NMUL, bool ADDMUL = false>
 __device__ __forceinline__ void threefry_rounds_m(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3,
-                                                  const uint32_t ks[5], const uint32_t *p2) {
+                                                  const uint32_t ks[5], const uint32_t *p2, uint32_t one = 1) {
 #define TF_RM(R)                                                                \
     if (R >= FIRST) {                                                           \
-        threefry_round_m<R, NMUL>(x0, x1, x2, x3, p2);                          \
+        threefry_round_m<R, NMUL, ADDMUL>(x0, x1, x2, x3, p2, one);             \
         if ((R + 1) % 4 == 0) threefry_inject<(R + 1) / 4>(x0, x1, x2, x3, ks); \
     }
     TF_RM(0) TF_RM(1) TF_RM(2) TF_RM(3) TF_RM(4) TF_RM(5) TF_RM(6) TF_RM(7) TF_RM(8) TF_RM(9)
@@ -316,6 +356,7 @@ struct ThreefryStream {
     uint32_t x3_0;  // rotl(ks3, 26) ^ x2_0 (round 0 x3)
     uint32_t x3r;   // rotl(x3_0, 11) (round 1)
     uint32_t p2[16];  // 2^R[r%8] multipliers for rotx<true>
+    uint32_t one;     // 1, opaque to the compiler (addp<true>)
 };
 
 inline ThreefryStream threefry_stream_setup(uint64_t seed, uint32_t sc) {
@@ -330,10 +371,11 @@ inline ThreefryStream threefry_stream_setup(uint64_t seed, uint32_t sc) {
     p.x3r = rotl32(p.x3_0, 11);
     const int ROT[8][2] = {{10, 26}, {11, 21}, {13, 27}, {23, 5}, {6, 20}, {17, 11}, {25, 10}, {18, 20}};
     for (int i = 0; i < 8; i++) { p.p2[2 * i] = 1u << ROT[i][0]; p.p2[2 * i + 1] = 1u << ROT[i][1]; }
+    p.one = 1;
     return p;
 }
 
-template <int NMUL = 0>
+template <int NMUL = 0, bool ADDMUL = false>
 __device__ __forceinline__ uint4 threefry_stream_block(const ThreefryStream& p, uint32_t bc) {
     // round 0 (even; rot 10, 26): x = (bc+ks0, ks1, ks2, ks3)
     uint32_t x0 = bc + p.s01;
@@ -344,7 +386,7 @@ __device__ __forceinline__ uint4 threefry_stream_block(const ThreefryStream& p, 
     uint32_t x3 = p.x3r ^ x0;
     uint32_t x2 = p.x2_0 + x1;
     x1 = rotl32(x1, 21) ^ x2;
-    threefry_rounds_m<2, NMUL>(x0, x1, x2, x3, p.ks, p.p2);
+    threefry_rounds_m<2, NMUL, ADDMUL>(x0, x1, x2, x3, p.ks, p.p2, p.one);
     return make_uint4(x0, x1, x2, x3);
 }
 

@@ -38,12 +38,15 @@ struct FillArgs {
     void *out1;
 };
 
-// V selects a code variant per algorithm; for Threefry it is the number of
-// rotations done on the multiplier (rotx<true>): V = 0, 1, 2 -> 0, 12, 20 of 40.
+// V selects a code variant per algorithm. Threefry: V = 0 compiler-scheduled;
+// V = 1: all round adds forced to IMAD + 10 of 40 rotations on the multiplier;
+// V = 2: all round adds forced to IMAD, rotations on the ALU.
 template <int ALG, int V>
 __device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, uint32_t bc) {
     if constexpr (ALG == PHILOX) return philox_stream_block(p, bc);
-    else return threefry_stream_block<V == 0 ? 0 : (V == 1 ? 12 : 20)>(p, bc);
+    else if constexpr (V == 0) return threefry_stream_block<0, false>(p, bc);
+    else if constexpr (V == 1) return threefry_stream_block<10, true>(p, bc);
+    else return threefry_stream_block<0, true>(p, bc);
 }
 
 template <int ALG, bool SKIP, int V = 0>
@@ -161,13 +164,14 @@ static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
     return check_launch("fill_kernel");
 }
 
-// Units per thread per tile. Default 2 (two independent cipher chains in
-// flight per thread on top of full occupancy); CBRNG_FILL_ILP=1|2|4 overrides
-// for tuning runs.
+// Units per thread per tile (independent cipher chains in flight per thread).
+// Defaults from the B200 sweep in profiles/r1c_tune.md: Philox 4, Threefry 2,
+// Squares 4. CBRNG_FILL_ILP=1|2|4 overrides for tuning runs.
+template <int ALG>
 static int fill_ilp() {
     static int v = [] {
         const char *e = getenv("CBRNG_FILL_ILP");
-        int x = e ? atoi(e) : 2;
+        int x = e ? atoi(e) : (ALG == THREEFRY ? 2 : 4);
         return (x == 1 || x == 2 || x == 4) ? x : 2;
     }();
     return v;
@@ -185,7 +189,7 @@ static int tf_variant() {
 
 template <int ALG, int OUT, bool SKIP, int V>
 static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
-    switch (fill_ilp()) {
+    switch (fill_ilp<ALG>()) {
         case 1: return launch_fill_ilp<ALG, OUT, SKIP, 1, V>(a, st);
         case 4: return launch_fill_ilp<ALG, OUT, SKIP, 4, V>(a, st);
         default: return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);

@@ -131,11 +131,22 @@ __global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_const
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t groups = a.nwords / 16, rem = a.nwords % 16;
     const bool vec = (a.nwords % 4) == 0;
+    uint4 *const my = tile[wib];
+    // Loop-invariant staging slots: lane writes row `lane`, chunk c at wslot(c);
+    // for the copy-out, lane reads row r = 8k + lane/4, chunk lane%4 at rslot + 32k
+    // (the swizzle term (r >> 1) & 3 = (lane >> 3) & 3 does not depend on k).
+    const uint32_t wx = (lane >> 1) & 3;
+    const uint32_t rrow = lane >> 2, rc = lane & 3;
+    const uint32_t rslot = rrow * TY_CH + (rc ^ ((lane >> 3) & 3));
     for (uint64_t s0 = warp * 32; s0 < a.n_streams; s0 += nwarps * 32) {
         const uint64_t sid = s0 + lane;
         const bool valid = sid < a.n_streams;
         uint4 st = tyche_init(valid ? seed_of(a, sid) : 0, valid ? ctr_of(a, sid) : 0);
         uint32_t A = st.x, B = st.y, C = st.z, D = st.w;
+        // output word index of (row rrow + 8k, chunk rc) in group 0
+        const uint64_t obase = (s0 + rrow) * a.nwords + rc * 4;
+        const uint64_t rstride = 8ull * a.nwords;
+        const uint32_t rows_left = a.n_streams - s0 < 32 ? (uint32_t)(a.n_streams - s0) : 32u;
         for (uint32_t g = 0; g < groups; g++) {
 #pragma unroll
             for (int c = 0; c < TY_CH; c++) {
@@ -144,15 +155,14 @@ __global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_const
                 tyche_mix(A, B, C, D); w.y = B;
                 tyche_mix(A, B, C, D); w.z = B;
                 tyche_mix(A, B, C, D); w.w = B;
-                tile[wib][ty_slot(lane, c)] = w;
+                my[lane * TY_CH + (c ^ wx)] = w;
             }
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < 4; k++) {
-                const uint32_t r = k * 8 + (lane >> 2), c = lane & 3;
-                if (s0 + r < a.n_streams) {
-                    const uint64_t at = (s0 + r) * a.nwords + g * 16 + c * 4;
-                    const uint4 v = tile[wib][ty_slot(r, c)];
+                if (rrow + 8 * k < rows_left) {
+                    const uint64_t at = obase + k * rstride + g * 16;
+                    const uint4 v = my[rslot + 32 * k];
                     if (vec) {
                         store4<OUT>(a.out, at, v);
                     } else {  // rows not 16-byte aligned (nwords % 4 != 0)
