@@ -172,6 +172,8 @@ def main() -> None:
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--quick", action="store_true", help="skip the side measurements")
     ap.add_argument("--no-side", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="process-group backend (gloo lets the N>1 logic run several ranks on one GPU for testing)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
@@ -185,10 +187,14 @@ def main() -> None:
     from paper_2310_19925_b200 import _lib, bulk, sharding
 
     rank, world, local = dist_env()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     lib = _lib.lib()
     stream = torch.cuda.current_stream(dev)
     sptr = int(stream.cuda_stream)
@@ -253,8 +259,21 @@ def main() -> None:
     prof = ROOT / "profiles" / "ncu_summary.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("traffic_bytes", {}).get(f"uniform_f32_{dom}")
-        except (ValueError, AttributeError):
+            summ = json.loads(prof.read_text())
+            traffic = summ.get("traffic_bytes", {}).get(f"uniform_f32_{dom}")
+            # the INT-pipe side of the roofline, from the committed ncu capture:
+            # the busiest of issue / ALU / FMA-heavy is the kernel's compute bound
+            pats = {"philox": "fill_kernel<0, 1", "threefry": "fill_kernel<1, 1", "squares": "fill_kernel<2, 1",
+                    "tyche": "tyche_prefix_kernel<1>"}
+            for a, pat in pats.items():
+                k = next((k for k in summ.get("kernels", []) if pat in k["kernel"]), None)
+                if k:
+                    pipes = {"issue": k.get("issue_active_pct"), "alu": k.get("alu_pct"),
+                             "fma_heavy": k.get("fmaheavy_pct")}
+                    bind = max(pipes, key=lambda p_: pipes[p_] or 0)
+                    per_gen[a]["ncu"] = {**{p_: round(v, 1) for p_, v in pipes.items() if v is not None},
+                                         "binding_pipe": bind, "source": f"profiles/{summ.get('tag')}_ncu.md"}
+        except (ValueError, AttributeError, KeyError):
             traffic = None
     roofline = {"bound": "hbm", "achieved": per_gen[dom]["hbm_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": per_gen[dom]["hbm_frac"], "traffic": traffic, "kernel": f"fill_kernel<{dom}, f32>",

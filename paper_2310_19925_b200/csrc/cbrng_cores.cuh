@@ -504,6 +504,14 @@ __host__ __device__ __forceinline__ uint4 tyche_init(uint64_t seed, uint32_t sc)
 // (w>>8)*2^-24 in double then casts, which is the same value).
 __device__ __forceinline__ float u32_to_f32(uint32_t w) { return (float)(w >> 8) * 0x1p-24f; }
 
+// Same map with the shift done as hi(w * 2^24) on the FMA-heavy pipe instead of
+// SHF on the ALU pipe, for ALU-bound generators (Threefry, Tyche). `m24` must
+// be the runtime value 1 << 24 (a kernel parameter), or the compiler folds the
+// multiply back into a shift.
+__device__ __forceinline__ float u32_to_f32_mul(uint32_t w, uint32_t m24) {
+    return (float)__umulhi(w, m24) * 0x1p-24f;
+}
+
 // uniform_f64: ((lo | hi<<32) >> 11) * 2^-53, low word first.
 __device__ __forceinline__ double u32x2_to_f64(uint32_t lo, uint32_t hi) {
     uint64_t u = ((uint64_t)hi << 32) | lo;

@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "cbrng_internal.cuh"
+#include "cbrng_bm.cuh"
 
 namespace cbrng {
 
@@ -36,6 +37,7 @@ struct FillArgs {
     uint64_t n_units;  // full units
     void *out0;
     void *out1;
+    uint32_t m24;      // 1 << 24 at run time (u32_to_f32_mul)
 };
 
 // V selects a code variant per algorithm. Threefry: V = 0 compiler-scheduled;
@@ -63,18 +65,24 @@ __device__ __forceinline__ uint4 unit_words(const typename StreamOf<ALG>::T &p, 
     }
 }
 
-template <int OUT>
-__device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w) {
+template <int OUT, bool MULSHIFT = false>
+__device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0) {
     if constexpr (OUT == OUT_U32) {
         __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
     } else if constexpr (OUT == OUT_F32) {
-        __stcs(reinterpret_cast<float4 *>(out0) + u,
-               make_float4(u32_to_f32(w.x), u32_to_f32(w.y), u32_to_f32(w.z), u32_to_f32(w.w)));
+        if constexpr (MULSHIFT) {
+            __stcs(reinterpret_cast<float4 *>(out0) + u,
+                   make_float4(u32_to_f32_mul(w.x, m24), u32_to_f32_mul(w.y, m24), u32_to_f32_mul(w.z, m24),
+                               u32_to_f32_mul(w.w, m24)));
+        } else {
+            __stcs(reinterpret_cast<float4 *>(out0) + u,
+                   make_float4(u32_to_f32(w.x), u32_to_f32(w.y), u32_to_f32(w.z), u32_to_f32(w.w)));
+        }
     } else if constexpr (OUT == OUT_F64) {
         __stcs(reinterpret_cast<double2 *>(out0) + u, make_double2(u32x2_to_f64(w.x, w.y), u32x2_to_f64(w.z, w.w)));
     } else {
         double z0, z1;
-        box_muller(w, z0, z1);
+        box_muller_fast(w, z0, z1);
         __stcs(reinterpret_cast<double *>(out0) + u, z0);
         __stcs(reinterpret_cast<double *>(out1) + u, z1);
     }
@@ -108,7 +116,7 @@ __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillA
 #pragma unroll
         for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, base + 32 * j);
 #pragma unroll
-        for (int j = 0; j < ILP; j++) store_unit<OUT>(a.out0, a.out1, base + 32 * j, w[j]);
+        for (int j = 0; j < ILP; j++) store_unit<OUT, ALG == THREEFRY>(a.out0, a.out1, base + 32 * j, w[j], a.m24);
     }
     // Remainder (< one tile) and the partial trailing unit: the last warp of the grid.
     if (warp == nwarps - 1) {
@@ -143,7 +151,7 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
             tyche_mix(a, b, c, d); w.z = b;
             tyche_mix(a, b, c, d); w.w = b;
             double z0, z1;
-            box_muller(w, z0, z1);
+            box_muller_fast(w, z0, z1);
             reinterpret_cast<double *>(out0)[i] = z0;
             reinterpret_cast<double *>(out1)[i] = z1;
         }
@@ -165,14 +173,17 @@ static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
 }
 
 // Units per thread per tile (independent cipher chains in flight per thread).
-// Defaults from the B200 sweep in profiles/r1c_tune.md: Philox 4, Threefry 2,
-// Squares 4. CBRNG_FILL_ILP=1|2|4 overrides for tuning runs.
-template <int ALG>
+// Defaults from the B200 sweeps in profiles/r1{c,d}_tune.md: 4 for every
+// algorithm. CBRNG_FILL_ILP=1|2|4 overrides for tuning runs.
+template <int ALG, int OUT>
 static int fill_ilp() {
     static int v = [] {
         const char *e = getenv("CBRNG_FILL_ILP");
-        int x = e ? atoi(e) : (ALG == THREEFRY ? 2 : 4);
-        return (x == 1 || x == 2 || x == 4) ? x : 2;
+        // Box-Muller is FP64-pipe work with ~60 live doubles per pair: one pair per
+        // thread per tile keeps it spill-free.
+        const int dflt = OUT == OUT_NORMAL ? 1 : 4;
+        int x = e ? atoi(e) : dflt;
+        return (x == 1 || x == 2 || x == 4) ? x : dflt;
     }();
     return v;
 }
@@ -181,15 +192,15 @@ static int fill_ilp() {
 static int tf_variant() {
     static int v = [] {
         const char *e = getenv("CBRNG_TF_VARIANT");
-        int x = e ? atoi(e) : 0;
-        return (x >= 0 && x <= 2) ? x : 0;
+        int x = e ? atoi(e) : 2;  // B200 sweep (profiles/r1d_tune.md): forced-IMAD adds
+        return (x >= 0 && x <= 2) ? x : 2;
     }();
     return v;
 }
 
 template <int ALG, int OUT, bool SKIP, int V>
 static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
-    switch (fill_ilp<ALG>()) {
+    switch (fill_ilp<ALG, OUT>()) {
         case 1: return launch_fill_ilp<ALG, OUT, SKIP, 1, V>(a, st);
         case 4: return launch_fill_ilp<ALG, OUT, SKIP, 4, V>(a, st);
         default: return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);
@@ -227,6 +238,7 @@ static int launch_fill(uint64_t seed, uint32_t sc, uint64_t word_pos, uint64_t n
     a.n_units = n_units;
     a.out0 = out0;
     a.out1 = out1;
+    a.m24 = 1u << 24;
     if (ALG != SQUARES && a.skip) return launch_fill_k<ALG, OUT, true>(a, st);
     return launch_fill_k<ALG, OUT, false>(a, st);
 }

@@ -24,6 +24,7 @@ struct PrefixArgs {
     uint32_t nwords;
     uint64_t n_streams;
     void *out;
+    uint32_t m24;  // 1 << 24 at run time (u32_to_f32_mul)
 };
 
 __device__ __forceinline__ uint64_t seed_of(const PrefixArgs &a, uint64_t i) {
@@ -71,9 +72,13 @@ __device__ __forceinline__ uint32_t single_word(const StreamKey<ALG> &k, uint32_
 
 // OUT: 0 = u32 words, 1 = uniform f32.
 template <int OUT>
-__device__ __forceinline__ void store4(void *out, uint64_t word_index, uint4 w) {
+__device__ __forceinline__ void store4(void *out, uint64_t word_index, uint4 w, uint32_t m24 = 0) {
     if constexpr (OUT == 0) {
         __stcs(reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(out) + word_index), w);
+    } else if (m24) {
+        __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + word_index),
+               make_float4(u32_to_f32_mul(w.x, m24), u32_to_f32_mul(w.y, m24), u32_to_f32_mul(w.z, m24),
+                           u32_to_f32_mul(w.w, m24)));
     } else {
         __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + word_index),
                make_float4(u32_to_f32(w.x), u32_to_f32(w.y), u32_to_f32(w.z), u32_to_f32(w.w)));
@@ -164,7 +169,7 @@ __global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_const
                     const uint64_t at = obase + k * rstride + g * 16;
                     const uint4 v = my[rslot + 32 * k];
                     if (vec) {
-                        store4<OUT>(a.out, at, v);
+                        store4<OUT>(a.out, at, v, a.m24);  // Tyche is ALU-bound: shift on the multiplier
                     } else {  // rows not 16-byte aligned (nwords % 4 != 0)
                         store1<OUT>(a.out, at, v.x); store1<OUT>(a.out, at + 1, v.y);
                         store1<OUT>(a.out, at + 2, v.z); store1<OUT>(a.out, at + 3, v.w);
@@ -205,7 +210,8 @@ static int dispatch_prefix(int alg, const uint64_t *seeds, uint64_t seed_base, c
         set_error("output pointer not 16-byte aligned");
         return CBRNG_EALIGN;
     }
-    PrefixArgs a{seeds, seed_base, ctrs, ctr_scalar, nwords, n_streams, out};
+    PrefixArgs a{seeds, seed_base, ctrs, ctr_scalar, nwords, n_streams, out, 0};
+    if (alg == TYCHE) a.m24 = 1u << 24;
     cudaStream_t st = as_stream(stream);
     switch (alg) {
         case PHILOX: return launch_prefix<PHILOX, OUT>(a, st);

@@ -338,3 +338,93 @@ class TestSpotChecksAtScale:
         small = whole[:1000].cpu().numpy()
         assert sharding.digest_words_np(small.reshape(-1), 0) == int(
             sharding.digest_words(whole[:1000], 0).cpu().numpy()[0]) % 2**64
+
+
+class TestApiSurface:
+    """Reference API behaviours (generators.py:227-406, distributions.py) on the CUDA path."""
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_copy_replays(self, cb, alg):
+        g = cb.make_generator(alg, 123456789, 42)
+        [g.next_u32() for _ in range(7)]
+        h = g.copy()
+        assert [g.next_u32() for _ in range(20)] == [h.next_u32() for _ in range(20)]
+        assert np.array_equal(host(g.words(300)), host(h.words(300)))
+
+    def test_generator_classes(self, cb, oracle):
+        for cls, alg in ((cb.Philox, "philox"), (cb.Threefry, "threefry"), (cb.Squares, "squares"), (cb.Tyche, "tyche")):
+            assert np.array_equal(host(cls(9, 2).words(77)), oracle.stream_words(alg, 9, 2, 77))
+
+    def test_state_layout(self, cb):
+        import struct
+
+        g = cb.make_generator("threefry", 0x1122334455667788, 0x99AABBCC)
+        [g.next_u32() for _ in range(6)]
+        tag, seed, sc, ic, pos = struct.unpack("<BQIIB", g.state_bytes())
+        assert (tag, seed, sc, ic, pos) == (1, 0x1122334455667788, 0x99AABBCC, 2, 2)
+
+    def test_single_word_algorithms_reject_cache_pos(self, cb):
+        import struct
+
+        with pytest.raises(ValueError):
+            cb.Generator.from_state_bytes(struct.pack("<BQIIB", 2, 1, 2, 3, 1))
+
+    def test_squares_uses_low_32_seed_bits(self, cb):
+        a = host(cb.make_generator("squares", 2**40 + 123, 0).words(64))
+        b = host(cb.make_generator("squares", (2**40 + 123) & M32, 0).words(64))
+        assert np.array_equal(a, b)
+
+    def test_device_and_out_placement(self, cb, oracle):
+        import torch
+
+        ref = oracle.stream_words("philox", 5, 1, 1000)
+        assert isinstance(cb.make_generator("philox", 5, 1).words(1000, device="cpu"), np.ndarray)
+        out = torch.empty(1000, dtype=torch.uint32, device="cuda")
+        assert cb.make_generator("philox", 5, 1).words(1000, out=out) is out
+        assert np.array_equal(out.cpu().numpy(), ref)
+        hout = np.empty(1000, np.uint32)
+        cb.make_generator("philox", 5, 1).words(1000, out=hout)
+        assert np.array_equal(hout, ref)
+        pinned = torch.empty(1000, dtype=torch.uint32, pin_memory=True)
+        cb.make_generator("philox", 5, 1).words(1000, out=pinned)
+        assert np.array_equal(pinned.numpy(), ref)
+
+    @pytest.mark.parametrize("alg", ["philox", "threefry", "squares", "tyche"])
+    def test_normal2_resumed_mid_stream(self, cb, oracle, alg):
+        g = cb.make_generator(alg, 8, 1)
+        [g.next_u32() for _ in range(3)]
+        z0, z1 = (host(z) for z in cb.normal2_array(g, 1001))
+        r0, r1 = oracle.words_to_normal2(oracle.stream_words(alg, 8, 1, 3 + 4 * 1001)[3:])
+        for got, r in ((z0, r0), (z1, r1)):
+            assert np.all(np.abs(got - r) <= BM_ULP * np.spacing(np.maximum(np.abs(r), 1.0)))
+        assert g._block_ctr == (1 + 1001 if alg in ("philox", "threefry") else 3 + 4 * 1001)
+
+    def test_draw_accounting(self, cb, oracle):
+        g = cb.make_generator("threefry", 8, 8)
+        w = oracle.stream_words("threefry", 8, 8, 16)
+        cb.uniform_f64(g); cb.uniform_f32(g); cb.draw_double2(g); cb.range_u32(g, 17); cb.normal2(g)
+        assert g.next_u32() == int(w[12])
+
+    def test_prefix_words_device_inputs(self, cb, oracle, golden_arrays):
+        import torch
+        from paper_2310_19925_b200 import bulk
+
+        seeds = torch.from_numpy(golden_arrays["prefix_seeds"]).cuda()
+        ctrs = torch.from_numpy(golden_arrays["prefix_ctrs"]).cuda()
+        got = bulk.prefix_words("threefry", seeds, ctrs, 19)
+        assert got.is_cuda
+        assert np.array_equal(got.cpu().numpy(), golden_arrays["prefix_threefry_19"])
+
+    def test_tyche_fill_c_abi(self, cb, oracle):
+        """_kernels.tyche_fill drop-in: state updated in place (synchronous)."""
+        import ctypes
+
+        import torch
+        from paper_2310_19925_b200 import _lib
+
+        st = np.array(oracle.tyche_init(77, 3), dtype=np.uint64)
+        out = torch.empty(1000, dtype=torch.uint32, device="cuda")
+        _lib.check(_lib.lib().cbrng_tyche_fill(st.ctypes.data, 1000, out.data_ptr(), None))
+        words, final = oracle.stream_words("tyche", 77, 3, 1000, tyche_state=oracle.tyche_init(77, 3))
+        assert np.array_equal(out.cpu().numpy(), words)
+        assert tuple(int(v) for v in st) == final
