@@ -68,6 +68,7 @@ CURAND_SIGNATURES = {
     "cbrng_curand_state_bytes": (u64, []),
     "cbrng_curand_brownian_init": (i32, [vp, u64, vp, vp, vp, vp, vp]),
     "cbrng_curand_brownian_steps": (i32, [vp, u64, vp, vp, vp, vp, u64, f64, f64, f64, i32, vp]),
+    "cbrng_probe_store": (i32, [vp, u64, i32, i32, vp]),
 }
 
 

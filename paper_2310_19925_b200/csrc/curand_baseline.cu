@@ -133,3 +133,41 @@ int cbrng_curand_brownian_steps(void *state, uint64_t n, double *x, double *y, d
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Store-bandwidth probe (measurement only): the write-only HBM ceiling for the
+// fill kernels' exact store pattern (resident grid, 4 x 16-byte streaming stores
+// per lane per tile). pattern 0 writes zeros (compressible), 1 writes
+// index*golden (incompressible, one IMAD per word) — B200's L2 compresses
+// zero-filled lines, so memset overstates what random data can reach.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) probe_store_kernel(uint4 *out, uint64_t n_units, int pattern) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = warp; t * 128 < n_units; t += nwarps) {
+        const uint64_t base = t * 128 + lane;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint64_t u = base + 32 * j;
+            if (u < n_units) {
+                const uint32_t v = (uint32_t)u * 0x9E3779B9u;
+                __stcs(out + u, pattern ? make_uint4(v, v ^ 0x5bd1e995u, v + 0x1b873593u, v * 3u)
+                                        : make_uint4(0u, 0u, 0u, 0u));
+            }
+        }
+    }
+}
+
+extern "C" int cbrng_probe_store(void *out, uint64_t n_bytes, int pattern, int blocks, void *stream) {
+    uint64_t n_units = n_bytes / 16;
+    if (blocks <= 0) {
+        int dev = 0, sms = 0, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, probe_store_kernel, 256, 0);
+        blocks = sms * occ;
+    }
+    probe_store_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>((uint4 *)out, n_units, pattern);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
