@@ -163,11 +163,26 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
 
 constexpr int FILL_BLOCK = 256;
 
+// Grid policy: CBRNG_GRID_MULT = k >= 1 launches k x the resident grid
+// (persistent, grid-stride); 0 launches one tile per warp (no persistence).
+static int grid_mult() {
+    static int v = [] {
+        const char *e = getenv("CBRNG_GRID_MULT");
+        int x = e ? atoi(e) : 1;
+        return x >= 0 ? x : 1;
+    }();
+    return v;
+}
+
 template <int ALG, int OUT, bool SKIP, int ILP, int V>
 static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
     auto k = fill_kernel<ALG, OUT, ILP, SKIP, V>;
     uint64_t work = (a.n_units + (FILL_BLOCK * ILP) - 1) / (FILL_BLOCK * ILP);
-    unsigned grid = grid_for(k, FILL_BLOCK, 0, work ? work : 1);
+    const int gm = grid_mult();
+    uint64_t g = gm == 0 ? work : (uint64_t)grid_for(k, FILL_BLOCK, 0, work ? work : 1) * gm;
+    if (g > work) g = work;
+    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
+    unsigned grid = (unsigned)(g ? g : 1);
     k<<<grid, FILL_BLOCK, 0, st>>>(a);
     return check_launch("fill_kernel");
 }

@@ -42,14 +42,15 @@ print(json.dumps(res))
 '''
 
 rows = []
-for ilp, tfv in itertools.product([2, 4], [0, 1, 2]):
-    env = dict(os.environ, CBRNG_FILL_ILP=str(ilp), CBRNG_TF_VARIANT=str(tfv))
+for ilp, gm in itertools.product([2, 4], [1, 2, 0]):
+    tfv = 2
+    env = dict(os.environ, CBRNG_FILL_ILP=str(ilp), CBRNG_TF_VARIANT=str(tfv), CBRNG_GRID_MULT=str(gm))
     r = subprocess.run([sys.executable, "-c", CHILD % str(ROOT)], env=env, capture_output=True, text=True)
     if r.returncode:
         print(r.stderr[-2000:])
         continue
     d = json.loads(r.stdout.strip().splitlines()[-1])
-    rows.append((ilp, tfv, d))
-    print(f"ILP={ilp} TF={tfv} " + " ".join(f"{k}={v['gbs']}" for k, v in d.items()), flush=True)
+    rows.append((ilp, gm, d))
+    print(f"ILP={ilp} GRID_MULT={gm} " + " ".join(f"{k}={v['gbs']}" for k, v in d.items()), flush=True)
 Path(ROOT / "gpurun_out").mkdir(exist_ok=True)
 (ROOT / "gpurun_out" / "tune_fills.json").write_text(json.dumps(rows, indent=1))
