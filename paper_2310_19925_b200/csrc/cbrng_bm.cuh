@@ -92,7 +92,12 @@ __device__ __forceinline__ double sqrt_fast(double a) {
 
 // sin(t), cos(t) for t in [0, 2*pi).
 __device__ __forceinline__ void sincos_2pi(double t, double &sn, double &cs) {
-    const double q = rint(t * c_bm.two_over_pi);
+    // quadrant q = nearest integer to t*2/pi via the 1.5*2^52 shifter: the
+    // integer lands in the low mantissa bits (no FRND/F2I round trip)
+    const double shifter = 0x1.8p52;
+    const double qs = fma(t, c_bm.two_over_pi, shifter);
+    const int qlo = __double2loint(qs);
+    const double q = qs - shifter;
     double x = fma(-q, c_bm.pio2_hi, t);
     x = fma(-q, c_bm.pio2_lo, x);
     const double z = x * x;
@@ -104,7 +109,7 @@ __device__ __forceinline__ void sincos_2pi(double t, double &sn, double &cs) {
                                      c_bm.c[1]), c_bm.c[0]);
     const double hz = 0.5 * z, wv = 1.0 - hz;
     const double cx = wv + (((1.0 - wv) - hz) + z * rc);
-    const int qi = (int)q & 3;
+    const int qi = qlo & 3;
     const double a = (qi & 1) ? cx : sx;  // sin(t)
     const double b = (qi & 1) ? sx : cx;  // cos(t)
     sn = (qi & 2) ? -a : a;

@@ -194,9 +194,9 @@ template <int ALG, int OUT>
 static int fill_ilp() {
     static int v = [] {
         const char *e = getenv("CBRNG_FILL_ILP");
-        // Box-Muller is FP64-pipe work with ~60 live doubles per pair: one pair per
-        // thread per tile keeps it spill-free.
-        const int dflt = OUT == OUT_NORMAL ? 1 : 4;
+        // Box-Muller: two pairs per thread hide the long FP64 dependency chains
+        // (ncu r1e at one pair: issue 64 %, "wait" the top stall).
+        const int dflt = OUT == OUT_NORMAL ? 2 : 4;
         int x = e ? atoi(e) : dflt;
         return (x == 1 || x == 2 || x == 4) ? x : dflt;
     }();

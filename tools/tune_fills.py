@@ -32,6 +32,10 @@ for a, nm in enumerate(["philox", "threefry", "squares"]):
 run("tyche_ms", lambda: _lib.check(L.cbrng_prefix_uniform_f32(3, None, 0, None, 0, 1 << 22, 256, out.data_ptr(), s)))
 run("philox_ms_u32", lambda: _lib.check(L.cbrng_prefix_words(0, None, 0, None, 0, 1 << 22, 256, out.data_ptr(), s)))
 run("memset", lambda: out.zero_())
+z0 = torch.empty(1 << 27, dtype=torch.float64, device="cuda"); z1 = torch.empty_like(z0)
+run("normal2_pairs", lambda: _lib.check(L.cbrng_normal2_f64(0, 42, 0, 0, None, 1 << 27, z0.data_ptr(), z1.data_ptr(), None, s)))
+res["normal2_pairs"]["gbs"] = round(res["normal2_pairs"]["gbs"] * 4, 1)  # 16 B per pair vs 4 B per f32 in run()
+del z0, z1
 from paper_2310_19925_b200 import brownian
 cfg = brownian.SimConfig(10_000_000, 200)
 p = brownian.init_particles(cfg)
