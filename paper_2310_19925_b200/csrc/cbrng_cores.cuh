@@ -84,7 +84,7 @@ struct PhiloxStream {
     uint32_t rk0[6], rk1[6];  // rounds 4..9
 };
 
-inline PhiloxStream philox_stream_setup(uint64_t seed, uint32_t sc) {
+__host__ __device__ inline PhiloxStream philox_stream_setup(uint64_t seed, uint32_t sc) {
     uint32_t K0[10], K1[10];
     K0[0] = (uint32_t)seed;
     K1[0] = (uint32_t)(seed >> 32);
@@ -359,7 +359,7 @@ struct ThreefryStream {
     uint32_t one;     // 1, opaque to the compiler (addp<true>)
 };
 
-inline ThreefryStream threefry_stream_setup(uint64_t seed, uint32_t sc) {
+__host__ __device__ inline ThreefryStream threefry_stream_setup(uint64_t seed, uint32_t sc) {
     ThreefryStream p;
     uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32), k2 = sc, k3 = 0;
     p.ks[0] = k0; p.ks[1] = k1; p.ks[2] = k2; p.ks[3] = k3;

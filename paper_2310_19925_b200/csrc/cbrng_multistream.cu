@@ -56,6 +56,26 @@ template <> struct StreamKey<SQUARES> {
     __device__ __forceinline__ uint4 block(uint32_t b) const { return squares_stream_word4(p, 4 * b); }
 };
 
+// Long rows (>= 128 words): a warp owns one stream, so the stream-only part of
+// the cipher (round keys, Philox rounds 0-3 / Threefry rounds 0-1) is folded
+// once per row and amortised over the row's blocks (philox_stream_setup is the
+// same fold the single-stream fills do on the host).
+template <int ALG> struct RowKey { using T = StreamKey<ALG>; };
+template <> struct RowKey<PHILOX> {
+    struct T {
+        PhiloxStream p;
+        __device__ __forceinline__ T(uint64_t seed, uint32_t c) : p(philox_stream_setup(seed, c)) {}
+        __device__ __forceinline__ uint4 block(uint32_t b) const { return philox_stream_block(p, b); }
+    };
+};
+template <> struct RowKey<THREEFRY> {
+    struct T {
+        ThreefryStream p;
+        __device__ __forceinline__ T(uint64_t seed, uint32_t c) : p(threefry_stream_setup(seed, c)) {}
+        __device__ __forceinline__ uint4 block(uint32_t b) const { return threefry_stream_block<0, false>(p, b); }
+    };
+};
+
 template <int ALG>
 __device__ __forceinline__ uint32_t single_word(const StreamKey<ALG> &k, uint32_t j) {
     if constexpr (ALG == SQUARES) {
@@ -99,11 +119,13 @@ __global__ void __launch_bounds__(256) prefix_kernel(const __grid_constant__ Pre
     const uint32_t cpr = a.nwords / CW;  // chunks per row
     if (cpr >= 32) {
         for (uint64_t row = warp; row < a.n_streams; row += nwarps) {
-            const StreamKey<ALG> k(seed_of(a, row), ctr_of(a, row));
             const uint64_t rbase = row * a.nwords;
-            for (uint32_t j = lane; j < cpr; j += 32) {
-                if constexpr (CW == 4) store4<OUT>(a.out, rbase + 4ull * j, k.block(j));
-                else store1<OUT>(a.out, rbase + j, single_word<ALG>(k, j));
+            if constexpr (CW == 4) {
+                const typename RowKey<ALG>::T k(seed_of(a, row), ctr_of(a, row));
+                for (uint32_t j = lane; j < cpr; j += 32) store4<OUT>(a.out, rbase + 4ull * j, k.block(j));
+            } else {
+                const StreamKey<ALG> k(seed_of(a, row), ctr_of(a, row));
+                for (uint32_t j = lane; j < cpr; j += 32) store1<OUT>(a.out, rbase + j, single_word<ALG>(k, j));
             }
         }
     } else {

@@ -34,7 +34,7 @@ run("philox_ms_u32", lambda: _lib.check(L.cbrng_prefix_words(0, None, 0, None, 0
 run("memset", lambda: out.zero_())
 z0 = torch.empty(1 << 27, dtype=torch.float64, device="cuda"); z1 = torch.empty_like(z0)
 run("normal2_pairs", lambda: _lib.check(L.cbrng_normal2_f64(0, 42, 0, 0, None, 1 << 27, z0.data_ptr(), z1.data_ptr(), None, s)))
-res["normal2_pairs"]["gbs"] = round(res["normal2_pairs"]["gbs"] * 4, 1)  # 16 B per pair vs 4 B per f32 in run()
+res["normal2_pairs"]["gbs"] = round(res["normal2_pairs"]["gbs"] / 2, 1)  # run() assumes 4 GiB; 2^27 pairs = 2 GiB
 del z0, z1
 from paper_2310_19925_b200 import brownian
 cfg = brownian.SimConfig(10_000_000, 200)
@@ -46,7 +46,9 @@ print(json.dumps(res))
 '''
 
 rows = []
-for ilp, gm in itertools.product([2, 4], [1, 2, 0]):
+GRID = [int(x) for x in os.environ.get("TUNE_GRID", "1,2,0").split(",")]
+ILPS = [int(x) for x in os.environ.get("TUNE_ILP", "2,4").split(",")]
+for ilp, gm in itertools.product(ILPS, GRID):
     tfv = 2
     env = dict(os.environ, CBRNG_FILL_ILP=str(ilp), CBRNG_TF_VARIANT=str(tfv), CBRNG_GRID_MULT=str(gm))
     r = subprocess.run([sys.executable, "-c", CHILD % str(ROOT)], env=env, capture_output=True, text=True)
