@@ -91,11 +91,11 @@ __device__ __forceinline__ uint32_t single_word(const StreamKey<ALG> &k, uint32_
 }
 
 // OUT: 0 = u32 words, 1 = uniform f32.
-template <int OUT>
+template <int OUT, bool MULSHIFT = false>
 __device__ __forceinline__ void store4(void *out, uint64_t word_index, uint4 w, uint32_t m24 = 0) {
     if constexpr (OUT == 0) {
         __stcs(reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(out) + word_index), w);
-    } else if (m24) {
+    } else if constexpr (MULSHIFT) {
         __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + word_index),
                make_float4(u32_to_f32_mul(w.x, m24), u32_to_f32_mul(w.y, m24), u32_to_f32_mul(w.z, m24),
                            u32_to_f32_mul(w.w, m24)));
@@ -150,14 +150,15 @@ constexpr int TY_CH = 4;     // staged 16-byte chunks per stream row = 16 words 
 // LDS.128 (8 lanes = 2 rows x 4 chunks) conflict-free, without padding.
 __device__ __forceinline__ uint32_t ty_slot(uint32_t r, uint32_t c) { return r * TY_CH + (c ^ ((r >> 1) & 3)); }
 
-template <int OUT>
+// VEC: rows are 16-byte aligned (nwords % 4 == 0) -> 128-bit stores. Both the
+// alignment case and the f32 map are compile-time so the copy-out is branch-free.
+template <int OUT, bool VEC>
 __global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_constant__ PrefixArgs a) {
     __shared__ uint4 tile[TY_WARPS][32 * TY_CH];  // 16 KB per CTA: 8 CTAs (64 warps) fit an SM
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t groups = a.nwords / 16, rem = a.nwords % 16;
-    const bool vec = (a.nwords % 4) == 0;
     uint4 *const my = tile[wib];
     // Loop-invariant staging slots: lane writes row `lane`, chunk c at wslot(c);
     // for the copy-out, lane reads row r = 8k + lane/4, chunk lane%4 at rslot + 32k
@@ -170,11 +171,11 @@ __global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_const
         const bool valid = sid < a.n_streams;
         uint4 st = tyche_init(valid ? seed_of(a, sid) : 0, valid ? ctr_of(a, sid) : 0);
         uint32_t A = st.x, B = st.y, C = st.z, D = st.w;
-        // output word index of (row rrow + 8k, chunk rc) in group 0
-        const uint64_t obase = (s0 + rrow) * a.nwords + rc * 4;
+        // output word index of (row rrow + 8k, chunk rc) in group g: obase + k*rstride + 16g
+        uint64_t at = (s0 + rrow) * a.nwords + rc * 4;
         const uint64_t rstride = 8ull * a.nwords;
         const uint32_t rows_left = a.n_streams - s0 < 32 ? (uint32_t)(a.n_streams - s0) : 32u;
-        for (uint32_t g = 0; g < groups; g++) {
+        for (uint32_t g = 0; g < groups; g++, at += 16) {
 #pragma unroll
             for (int c = 0; c < TY_CH; c++) {
                 uint4 w;
@@ -188,13 +189,13 @@ __global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_const
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 if (rrow + 8 * k < rows_left) {
-                    const uint64_t at = obase + k * rstride + g * 16;
                     const uint4 v = my[rslot + 32 * k];
-                    if (vec) {
-                        store4<OUT>(a.out, at, v, a.m24);  // Tyche is ALU-bound: shift on the multiplier
+                    if constexpr (VEC) {
+                        store4<OUT, true>(a.out, at + k * rstride, v, a.m24);  // ALU-bound: shift on the multiplier
                     } else {  // rows not 16-byte aligned (nwords % 4 != 0)
-                        store1<OUT>(a.out, at, v.x); store1<OUT>(a.out, at + 1, v.y);
-                        store1<OUT>(a.out, at + 2, v.z); store1<OUT>(a.out, at + 3, v.w);
+                        const uint64_t o = at + k * rstride;
+                        store1<OUT>(a.out, o, v.x); store1<OUT>(a.out, o + 1, v.y);
+                        store1<OUT>(a.out, o + 2, v.z); store1<OUT>(a.out, o + 3, v.w);
                     }
                 }
             }
@@ -244,8 +245,13 @@ static int dispatch_prefix(int alg, const uint64_t *seeds, uint64_t seed_base, c
                 set_error("output pointer not 16-byte aligned");
                 return CBRNG_EALIGN;
             }
-            auto k = tyche_prefix_kernel<OUT>;
-            k<<<grid_for(k, 256, 0, (n_streams + 255) / 256), 256, 0, st>>>(a);
+            if (nwords % 4 == 0) {
+                auto k = tyche_prefix_kernel<OUT, true>;
+                k<<<grid_for(k, 256, 0, (n_streams + 255) / 256), 256, 0, st>>>(a);
+            } else {
+                auto k = tyche_prefix_kernel<OUT, false>;
+                k<<<grid_for(k, 256, 0, (n_streams + 255) / 256), 256, 0, st>>>(a);
+            }
             return check_launch("tyche_prefix_kernel");
         }
     }
