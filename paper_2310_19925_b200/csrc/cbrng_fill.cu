@@ -42,13 +42,15 @@ struct FillArgs {
 
 // V selects a code variant per algorithm. Threefry: V = 0 compiler-scheduled;
 // V = 1: all round adds forced to IMAD + 10 of 40 rotations on the multiplier;
-// V = 2: all round adds forced to IMAD, rotations on the ALU.
+// V = 2: all round adds forced to IMAD, rotations on the ALU;
+// V = 3: all round adds forced to IMAD + 6 rotations on the multiplier.
 template <int ALG, int V>
 __device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, uint32_t bc) {
     if constexpr (ALG == PHILOX) return philox_stream_block(p, bc);
     else if constexpr (V == 0) return threefry_stream_block<0, false>(p, bc);
     else if constexpr (V == 1) return threefry_stream_block<10, true>(p, bc);
-    else return threefry_stream_block<0, true>(p, bc);
+    else if constexpr (V == 2) return threefry_stream_block<0, true>(p, bc);
+    else return threefry_stream_block<6, true>(p, bc);
 }
 
 template <int ALG, bool SKIP, int V = 0>
@@ -210,7 +212,7 @@ static int tf_variant() {
     static int v = [] {
         const char *e = getenv("CBRNG_TF_VARIANT");
         int x = e ? atoi(e) : 2;  // B200 sweep (profiles/r1d_tune.md): forced-IMAD adds
-        return (x >= 0 && x <= 2) ? x : 2;
+        return (x >= 0 && x <= 3) ? x : 2;
     }();
     return v;
 }
@@ -230,6 +232,7 @@ static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
         switch (tf_variant()) {
             case 1: return launch_fill_v<ALG, OUT, SKIP, 1>(a, st);
             case 2: return launch_fill_v<ALG, OUT, SKIP, 2>(a, st);
+            case 3: return launch_fill_v<ALG, OUT, SKIP, 3>(a, st);
             default: break;
         }
     }
