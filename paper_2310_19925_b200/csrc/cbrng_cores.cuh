@@ -472,8 +472,9 @@ __device__ __forceinline__ uint32_t squares_stream_word(const SquaresStream &p, 
 
 // Words bc..bc+3 (counters wrap mod 2^32 in the low half only, bulk.py:268): the
 // incremental form is exact unless bc+k wraps, which the caller checks.
+template <bool NOWRAP = false>
 __device__ __forceinline__ uint4 squares_stream_word4(const SquaresStream &p, uint32_t bc) {
-    if (bc > 0xFFFFFFFCu) {
+    if (!NOWRAP && bc > 0xFFFFFFFCu) {
         return make_uint4(squares_stream_word(p, bc), squares_stream_word(p, bc + 1), squares_stream_word(p, bc + 2),
                           squares_stream_word(p, bc + 3));
     }
@@ -503,6 +504,15 @@ __host__ __device__ __forceinline__ uint4 tyche_init(uint64_t seed, uint32_t sc)
 // uniform_f32: (w >> 8) * 2^-24 (exact in float; the reference rounds
 // (w>>8)*2^-24 in double then casts, which is the same value).
 __device__ __forceinline__ float u32_to_f32(uint32_t w) { return (float)(w >> 8) * 0x1p-24f; }
+
+// Same map with no FP multiply: float(m) for m = w >> 8 < 2^24 is exact, and
+// scaling by 2^-24 is an exponent decrement (bits - (24 << 23)) for m != 0; the
+// signed max with 0 maps m = 0 to +0.0f. Three ALU ops instead of an FMUL on the
+// FMA-heavy pipe — used by the heavy-bound Squares fill.
+__device__ __forceinline__ float u32_to_f32_alu(uint32_t w) {
+    const int b = __float_as_int((float)(w >> 8)) - (24 << 23);
+    return __int_as_float(max(b, 0));
+}
 
 // Same map with the shift done as hi(w * 2^24) on the FMA-heavy pipe instead of
 // SHF on the ALU pipe, for ALU-bound generators (Threefry, Tyche). `m24` must

@@ -56,7 +56,8 @@ __device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, ui
 template <int ALG, bool SKIP, int V = 0>
 __device__ __forceinline__ uint4 unit_words(const typename StreamOf<ALG>::T &p, uint32_t bc0, uint32_t skip, uint64_t u) {
     if constexpr (ALG == SQUARES) {
-        return squares_stream_word4(p, bc0 + 4u * (uint32_t)u);
+        // V == 1: the host proved the fill never wraps the 32-bit counter
+        return squares_stream_word4<V == 1>(p, bc0 + 4u * (uint32_t)u);
     } else if constexpr (!SKIP) {
         return block_at<ALG, V>(p, bc0 + (uint32_t)u);
     } else {
@@ -67,12 +68,17 @@ __device__ __forceinline__ uint4 unit_words(const typename StreamOf<ALG>::T &p, 
     }
 }
 
-template <int OUT, bool MULSHIFT = false>
+// MULSHIFT: 0 = shift + FMUL, 1 = shift on the multiplier (ALU-bound kernels),
+// 2 = exponent arithmetic on the ALU (FMA-heavy-bound kernels).
+template <int OUT, int MULSHIFT = 0>
 __device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0) {
     if constexpr (OUT == OUT_U32) {
         __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
     } else if constexpr (OUT == OUT_F32) {
-        if constexpr (MULSHIFT) {
+        if constexpr (MULSHIFT == 2) {
+            __stcs(reinterpret_cast<float4 *>(out0) + u,
+                   make_float4(u32_to_f32_alu(w.x), u32_to_f32_alu(w.y), u32_to_f32_alu(w.z), u32_to_f32_alu(w.w)));
+        } else if constexpr (MULSHIFT == 1) {
             __stcs(reinterpret_cast<float4 *>(out0) + u,
                    make_float4(u32_to_f32_mul(w.x, m24), u32_to_f32_mul(w.y, m24), u32_to_f32_mul(w.z, m24),
                                u32_to_f32_mul(w.w, m24)));
@@ -118,7 +124,8 @@ __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillA
 #pragma unroll
         for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, base + 32 * j);
 #pragma unroll
-        for (int j = 0; j < ILP; j++) store_unit<OUT, ALG == THREEFRY>(a.out0, a.out1, base + 32 * j, w[j], a.m24);
+        for (int j = 0; j < ILP; j++)
+            store_unit<OUT, ALG == THREEFRY ? 1 : (ALG == SQUARES ? 2 : 0)>(a.out0, a.out1, base + 32 * j, w[j], a.m24);
     }
     // Remainder (< one tile) and the partial trailing unit: the last warp of the grid.
     if (warp == nwarps - 1) {
@@ -165,28 +172,11 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
 
 constexpr int FILL_BLOCK = 256;
 
-// Grid policy: CBRNG_GRID_MULT = k >= 1 launches k x the resident grid
-// (grid-stride); 0 launches one tile per warp. Default 8: the write-only probe
-// (tools/probe_store.py) reaches 6.2 TB/s with a resident persistent grid and
-// 7.2 TB/s with 16x, and the fills gain 1-2 % at 8x (profiles/r1g_tune.md).
-static int grid_mult() {
-    static int v = [] {
-        const char *e = getenv("CBRNG_GRID_MULT");
-        int x = e ? atoi(e) : 8;
-        return x >= 0 ? x : 8;
-    }();
-    return v;
-}
-
 template <int ALG, int OUT, bool SKIP, int ILP, int V>
 static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
     auto k = fill_kernel<ALG, OUT, ILP, SKIP, V>;
     uint64_t work = (a.n_units + (FILL_BLOCK * ILP) - 1) / (FILL_BLOCK * ILP);
-    const int gm = grid_mult();
-    uint64_t g = gm == 0 ? work : (uint64_t)grid_for(k, FILL_BLOCK, 0, work ? work : 1) * gm;
-    if (g > work) g = work;
-    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
-    unsigned grid = (unsigned)(g ? g : 1);
+    unsigned grid = grid_for(k, FILL_BLOCK, 0, work ? work : 1);
     k<<<grid, FILL_BLOCK, 0, st>>>(a);
     return check_launch("fill_kernel");
 }
@@ -228,6 +218,11 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
 
 template <int ALG, int OUT, bool SKIP>
 static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
+    if constexpr (ALG == SQUARES) {
+        // counters bc0 .. bc0 + 4*(n_units+1) - 1 never wrap: drop the per-unit check
+        if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) return launch_fill_v<ALG, OUT, SKIP, 1>(a, st);
+        return launch_fill_v<ALG, OUT, SKIP, 0>(a, st);
+    }
     if constexpr (ALG == THREEFRY) {
         switch (tf_variant()) {
             case 1: return launch_fill_v<ALG, OUT, SKIP, 1>(a, st);

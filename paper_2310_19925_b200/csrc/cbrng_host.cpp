@@ -3,6 +3,7 @@
 // (_kernels.py:89-96), which is sequential by definition and stays on the host.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -23,6 +24,15 @@ void set_error(const char *fmt, ...) {
 }
 
 void clear_error() { g_err[0] = 0; }
+
+int grid_mult() {
+    static int v = [] {
+        const char *e = getenv("CBRNG_GRID_MULT");
+        int x = e ? atoi(e) : 8;
+        return x >= 0 ? x : 8;
+    }();
+    return v;
+}
 
 int resident_blocks(const void *kernel, int block, size_t smem) {
     static std::mutex mu;

@@ -38,10 +38,20 @@ inline int check_cuda(cudaError_t e, const char *what) {
 // CTAs (cached per kernel x device), capped by the amount of work.
 int resident_blocks(const void *kernel, int block, size_t smem);
 
+// Grid policy for the streaming kernels: CBRNG_GRID_MULT = k >= 1 launches k x
+// the resident grid (grid-stride); 0 launches one tile per warp. Default 8: the
+// write-only probe (tools/probe_store.py) reaches 6.2 TB/s from a resident
+// persistent grid (ncu: warps active ~60 % of theoretical) and 7.18 TB/s from a
+// 16x grid; the fills gain 1-2 % and reach 95 % warps active at 8x
+// (profiles/r1g_tune.md, profiles/r1h_ncu.md).
+int grid_mult();
+
 template <typename K>
 inline unsigned grid_for(K kernel, int block, size_t smem, uint64_t work_blocks) {
-    uint64_t g = (uint64_t)resident_blocks(reinterpret_cast<const void *>(kernel), block, smem);
+    const int gm = grid_mult();
+    uint64_t g = gm == 0 ? work_blocks : (uint64_t)resident_blocks(reinterpret_cast<const void *>(kernel), block, smem) * gm;
     if (work_blocks < g) g = work_blocks;
+    if (g > 0x7FFFFFFFull) g = 0x7FFFFFFFull;
     if (g < 1) g = 1;
     return (unsigned)g;
 }

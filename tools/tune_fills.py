@@ -48,15 +48,15 @@ print(json.dumps(res))
 rows = []
 GRID = [int(x) for x in os.environ.get("TUNE_GRID", "1,2,0").split(",")]
 ILPS = [int(x) for x in os.environ.get("TUNE_ILP", "2,4").split(",")]
-for ilp, gm in itertools.product(ILPS, GRID):
-    tfv = 2
+TFV = [int(x) for x in os.environ.get("TUNE_TF", "2").split(",")]
+for ilp, gm, tfv in itertools.product(ILPS, GRID, TFV):
     env = dict(os.environ, CBRNG_FILL_ILP=str(ilp), CBRNG_TF_VARIANT=str(tfv), CBRNG_GRID_MULT=str(gm))
     r = subprocess.run([sys.executable, "-c", CHILD % str(ROOT)], env=env, capture_output=True, text=True)
     if r.returncode:
         print(r.stderr[-2000:])
         continue
     d = json.loads(r.stdout.strip().splitlines()[-1])
-    rows.append((ilp, gm, d))
-    print(f"ILP={ilp} GRID_MULT={gm} " + " ".join(f"{k}={v['gbs']}" for k, v in d.items()), flush=True)
+    rows.append((ilp, gm, tfv, d))
+    print(f"ILP={ilp} GRID_MULT={gm} TF={tfv} " + " ".join(f"{k}={v['gbs']}" for k, v in d.items()), flush=True)
 Path(ROOT / "gpurun_out").mkdir(exist_ok=True)
 (ROOT / "gpurun_out" / "tune_fills.json").write_text(json.dumps(rows, indent=1))
