@@ -413,12 +413,21 @@ __host__ __device__ __forceinline__ uint32_t squares_round(uint64_t key, uint64_
 }
 
 // One squaring step on 32-bit halves: (h, l) <- swap32((h:l)^2 + a) mod 2^64.
-// (h:l)^2 mod 2^64 = l*l + ((2*h*l) << 32): one IMAD.WIDE.U32 with the 64-bit
-// addend folded in, plus one IMAD for the cross term (h+h on the ALU pipe). The
-// generic 64-bit product costs IMAD.WIDE + 2 IMAD on the FMA-heavy pipe.
+// (h:l)^2 mod 2^64 = l*l + ((2*h*l) << 32). Pipe budget per squaring (the
+// kernel is FMA-heavy-bound): one IMAD.WIDE.U32 with the 64-bit addend folded
+// in, one IMAD for l*h, and the doubling folded into a 3-input IADD3
+// (hi + t + t) on the ALU pipe. Written naturally, ptxas emits l*(h+h) and puts
+// about half of the h+h adds on the heavy pipe (profiles/r1h SASS).
+__device__ __forceinline__ uint32_t mul_lo_opaque(uint32_t a, uint32_t b) {
+    uint32_t t;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(t) : "r"(a), "r"(b));
+    return t;
+}
+
 __device__ __forceinline__ void squares_sq_swap(uint32_t &h, uint32_t &l, uint64_t a) {
     const uint64_t p = (uint64_t)l * l + a;
-    const uint32_t hi = (uint32_t)(p >> 32) + l * (h + h);
+    const uint32_t t = mul_lo_opaque(l, h);
+    const uint32_t hi = (uint32_t)(p >> 32) + t + t;
     h = (uint32_t)p;  // swap32: the low half becomes the high half
     l = hi;
 }
@@ -432,7 +441,8 @@ __device__ __forceinline__ uint32_t squares_from_x(uint64_t x, uint64_t key) {
     squares_sq_swap(h, l, y);
     // last round: only the high half of x*x + z
     const uint64_t p = (uint64_t)l * l + z;
-    return (uint32_t)(p >> 32) + l * (h + h);
+    const uint32_t t = mul_lo_opaque(l, h);
+    return (uint32_t)(p >> 32) + t + t;
 }
 
 // Four consecutive counters c..c+3 of one key: x_{k+1} = x_k + key (64-bit add on

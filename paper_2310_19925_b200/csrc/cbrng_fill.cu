@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillA
         for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, base + 32 * j);
 #pragma unroll
         for (int j = 0; j < ILP; j++)
-            store_unit<OUT, ALG == THREEFRY ? 1 : (ALG == SQUARES ? 2 : 0)>(a.out0, a.out1, base + 32 * j, w[j], a.m24);
+            store_unit<OUT, ALG == THREEFRY ? 1 : 0>(a.out0, a.out1, base + 32 * j, w[j], a.m24);
     }
     // Remainder (< one tile) and the partial trailing unit: the last warp of the grid.
     if (warp == nwarps - 1) {
