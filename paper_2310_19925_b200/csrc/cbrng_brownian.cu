@@ -19,6 +19,7 @@
 //   vx -= ((gamma/mass) * vx) * dt;  vx += (r * 2.0 - 1.0) * sqrt(dt);  x += vx * dt
 // with every operation an explicit round-to-nearest intrinsic (no FMA contraction).
 #include <cmath>
+#include <cstdlib>
 
 #include "cbrng_internal.cuh"
 
@@ -147,8 +148,11 @@ __device__ __forceinline__ void step_update(double &x, double &y, double &vx, do
     y = __dadd_rn(y, __dmul_rn(vy, a.dt));
 }
 
-template <int ALG, bool HI0, bool FOLD>
-__global__ void __launch_bounds__(256) brownian_steps_kernel(const __grid_constant__ BrownArgs a) {
+// MINB: minimum resident CTAs per SM requested from ptxas (register cap). The
+// fused kernel is latency-bound on the Philox chain at 5 CTAs (44 registers,
+// ncu: issue 55 %, FMA-heavy 66 %); 6 CTAs cap it at 40 registers.
+template <int ALG, bool HI0, bool FOLD, int MINB>
+__global__ void __launch_bounds__(256, MINB) brownian_steps_kernel(const __grid_constant__ BrownArgs a) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t pid = a.pid ? a.pid[i] : a.pid_base + i;
         double x = a.x[i], y = a.y[i], vx = a.vx[i], vy = a.vy[i];
@@ -215,9 +219,17 @@ __global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint
     }
 }
 
-template <int ALG, bool HI0, bool FOLD>
-static int launch_steps_k(BrownArgs a, int mode, cudaStream_t st) {
-    auto k = brownian_steps_kernel<ALG, HI0, FOLD>;
+static int brownian_minb() {
+    static int v = [] {
+        const char *e = getenv("CBRNG_BROWNIAN_MINB");
+        return e && atoi(e) == 5 ? 5 : 6;
+    }();
+    return v;
+}
+
+template <int ALG, bool HI0, bool FOLD, int MINB>
+static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
+    auto k = brownian_steps_kernel<ALG, HI0, FOLD, MINB>;
     // One thread per particle: the fused kernel needs every particle resident
     // or queued, so the grid covers n (no persistence).
     const unsigned grid = (unsigned)((a.n + 255) / 256);
@@ -230,6 +242,16 @@ static int launch_steps_k(BrownArgs a, int mode, cudaStream_t st) {
         done += a.nsteps;
     }
     return check_launch("brownian_steps_kernel");
+}
+
+template <int ALG, bool HI0, bool FOLD>
+static int launch_steps_k(BrownArgs a, int mode, cudaStream_t st) {
+    if constexpr (!HI0) {
+        return launch_steps_kb<ALG, HI0, FOLD, 1>(a, mode, st);  // 64-bit pids: 20 live round keys, no cap
+    } else {
+        if (brownian_minb() == 5) return launch_steps_kb<ALG, HI0, FOLD, 5>(a, mode, st);
+        return launch_steps_kb<ALG, HI0, FOLD, 6>(a, mode, st);
+    }
 }
 
 template <int ALG>
