@@ -150,7 +150,8 @@ __device__ __forceinline__ void step_update(double &x, double &y, double &vx, do
 
 // MINB: minimum resident CTAs per SM requested from ptxas (register cap). The
 // fused kernel is latency-bound on the Philox chain at 5 CTAs (44 registers,
-// ncu: issue 55 %, FMA-heavy 66 %); 6 CTAs cap it at 40 registers.
+// ncu: issue 55 %, FMA-heavy 66 %); capping at 6 CTAs (40 registers) measured
+// slower (3.27e11 vs 3.40e11 p-steps/s), so 5 is the default.
 template <int ALG, bool HI0, bool FOLD, int MINB>
 __global__ void __launch_bounds__(256, MINB) brownian_steps_kernel(const __grid_constant__ BrownArgs a) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint
 static int brownian_minb() {
     static int v = [] {
         const char *e = getenv("CBRNG_BROWNIAN_MINB");
-        return e && atoi(e) == 5 ? 5 : 6;
+        return e && atoi(e) == 6 ? 6 : 5;  // 5 measured faster (profiles/r1j_tune.md)
     }();
     return v;
 }

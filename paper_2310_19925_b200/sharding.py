@@ -103,3 +103,44 @@ def digest_words_np(words: np.ndarray, global_offset: int) -> int:
     idx = np.arange(global_offset, global_offset + words.size, dtype=np.uint64)
     with np.errstate(over="ignore"):
         return int(np.sum(mix64_np(mix64_np(idx) ^ words.astype(np.uint64)), dtype=np.uint64))
+
+
+# ---------------------------------------------------------------------------
+# Rank-local entry points (one process per GPU; `rank`/`world` from torchrun)
+# ---------------------------------------------------------------------------
+
+def uniform_f32_shard(alg, seed: int, stream_ctr: int, n_total: int, rank: int, world: int, out=None):
+    """This rank's slice [lo, hi) of uniform_f32_array(make_generator(alg, seed, ctr), n_total):
+    a contiguous counter range cut on 4-word boundaries, filled with no communication.
+    Returns (lo, hi, tensor). Tyche is serial within a stream and cannot be cut."""
+    alg = as_algorithm(alg)
+    if alg is Algorithm.TYCHE:
+        raise ValueError("Tyche is sequential within a stream; shard Tyche work across streams instead")
+    lo, hi = shard_range(n_total, rank, world, align=4)
+    t = out if out is not None else torch.empty(hi - lo, dtype=torch.float32, device=_dev.cuda_device())
+    if hi > lo:
+        _lib.check(_lib.lib().cbrng_uniform_f32(int(alg), seed, stream_ctr & MASK32, lo, None, hi - lo, t.data_ptr(),
+                                                None, _dev.sptr(t)), "uniform_f32")
+    return lo, hi, t
+
+
+def prefix_words_shard(alg, n_streams: int, nwords: int, ctr: int, rank: int, world: int, seed_base: int = 0):
+    """This rank's rows [lo, hi) of prefix_words(alg, arange(seed_base, seed_base + n_streams), ctr, nwords)."""
+    from . import bulk
+
+    lo, hi = shard_range(n_streams, rank, world)
+    return lo, hi, bulk.prefix_words(alg, range(seed_base + lo, seed_base + hi), ctr, nwords)
+
+
+def run_sim_shard(cfg, rank: int, world: int):
+    """Brownian walk on this rank's pid range; returns (particles, stats) with the
+    int64 statistics all-reduced over ranks (identical for any world size)."""
+    from . import brownian
+
+    lo, hi = shard_range(cfg.n_particles, rank, world)
+    p = brownian.init_particles(cfg, pid_base=lo, n=hi - lo)
+    if cfg.steps:
+        brownian.run_steps(p, cfg)
+    acc = brownian.stats(p) if hi > lo else torch.zeros(8, dtype=torch.int64, device=_dev.cuda_device())
+    allreduce_sum_(acc)
+    return p, acc

@@ -428,3 +428,44 @@ class TestApiSurface:
         words, final = oracle.stream_words("tyche", 77, 3, 1000, tyche_state=oracle.tyche_init(77, 3))
         assert np.array_equal(out.cpu().numpy(), words)
         assert tuple(int(v) for v in st) == final
+
+
+class TestShardingAndKernelsModule:
+    def test_uniform_f32_shards_concatenate(self, cb, oracle):
+        import torch
+        from paper_2310_19925_b200 import sharding
+
+        n = (1 << 20) + 6
+        whole = cb.uniform_f32_array(cb.make_generator("threefry", 42, 3), n)
+        for world in (1, 2, 3, 8):
+            parts = [sharding.uniform_f32_shard("threefry", 42, 3, n, r, world)[2] for r in range(world)]
+            assert torch.equal(torch.cat(parts), whole)
+
+    def test_run_sim_shard_stats_invariant(self, cb):
+        import torch
+        from paper_2310_19925_b200 import sharding
+
+        cfg = cb.SimConfig(5003, 30)
+        accs = []
+        for world in (1, 4):
+            acc = torch.zeros(8, dtype=torch.int64, device="cuda")
+            for r in range(world):
+                _, a = sharding.run_sim_shard(cfg, r, world)  # no process group: local sums
+                acc += a
+            accs.append(acc)
+        assert torch.equal(accs[0], accs[1])
+
+    def test_kernels_module_drop_in(self, cb, oracle):
+        from paper_2310_19925_b200 import _kernels
+
+        st = np.array(oracle.tyche_init(77, 3), dtype=np.uint64)
+        out = np.empty(333, np.uint32)
+        _kernels.tyche_fill(st, out)
+        words, final = oracle.stream_words("tyche", 77, 3, 333, tyche_state=oracle.tyche_init(77, 3))
+        assert np.array_equal(out, words) and tuple(int(v) for v in st) == final
+        seeds = np.arange(10, 20, dtype=np.uint64)
+        scs = np.full(10, 4, np.uint64)
+        blk = np.empty((10, 4), np.uint32)
+        _kernels.philox_block_lanes(seeds, scs, 1, blk)
+        assert np.array_equal(blk, oracle.prefix_words("philox", seeds, 4, 8)[:, 4:8])
+        assert _kernels.fnv1a64(np.zeros(40, np.uint8)) == oracle.fnv1a64(bytes(40))
