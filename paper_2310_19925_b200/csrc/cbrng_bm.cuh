@@ -80,14 +80,16 @@ __device__ __forceinline__ double log_unit(double x) {
     return fma(dk, c_bm.ln2_hi, -((hfsq - fma(s, hfsq + R, dk * c_bm.ln2_lo)) - f));
 }
 
-// sqrt(a), a >= 0 finite.
+// sqrt(a), a >= 0 finite. a = 0 (u1 == 1) must give 0: the rsqrt input is
+// clamped to the smallest normal on the high word (one integer max, no FP
+// compare/select), so y stays finite and r = a*y = 0 exactly.
 __device__ __forceinline__ double sqrt_fast(double a) {
-    double y = rsqrt_approx(a);
+    const double ac = __hiloint2double(max(__double2hiint(a), 0x00100000), __double2loint(a));
+    double y = rsqrt_approx(ac);
     y = y * fma(-0.5 * a * y, y, 1.5);
     y = y * fma(-0.5 * a * y, y, 1.5);
-    double r = a * y;
-    r = fma(0.5 * y, fma(-r, r, a), r);  // residual correction
-    return a == 0.0 ? 0.0 : r;
+    const double r = a * y;
+    return fma(0.5 * y, fma(-r, r, a), r);  // residual correction
 }
 
 // sin(t), cos(t) for t in [0, 2*pi).
@@ -109,11 +111,14 @@ __device__ __forceinline__ void sincos_2pi(double t, double &sn, double &cs) {
                                      c_bm.c[1]), c_bm.c[0]);
     const double hz = 0.5 * z, wv = 1.0 - hz;
     const double cx = wv + (((1.0 - wv) - hz) + z * rc);
-    const int qi = qlo & 3;
-    const double a = (qi & 1) ? cx : sx;  // sin(t)
-    const double b = (qi & 1) ? sx : cx;  // cos(t)
-    sn = (qi & 2) ? -a : a;
-    cs = ((qi + 1) & 2) ? -b : b;
+    // quadrant: odd q swaps sin/cos; the signs are xor-ed into the high words
+    const bool odd = qlo & 1;
+    const double a = odd ? cx : sx;  // |sin(t)| up to sign
+    const double b = odd ? sx : cx;  // |cos(t)| up to sign
+    const int ssgn = (qlo << 30) & 0x80000000;        // q & 2
+    const int csgn = ((qlo + 1) << 30) & 0x80000000;  // (q + 1) & 2
+    sn = __hiloint2double(__double2hiint(a) ^ ssgn, __double2loint(a));
+    cs = __hiloint2double(__double2hiint(b) ^ csgn, __double2loint(b));
 }
 
 __device__ __forceinline__ void box_muller_fast(uint4 w, double &z0, double &z1) {
