@@ -278,6 +278,12 @@ def main() -> None:
     roofline = {"bound": "hbm", "achieved": per_gen[dom]["hbm_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": per_gen[dom]["hbm_frac"], "traffic": traffic, "kernel": f"fill_kernel<{dom}, f32>",
                 "algorithmic_bytes_per_launch": bytes_per_fill, "peak_source": pk["source"]}
+    if "ncu" in per_gen[dom]:
+        # the slower of the two rooflines binds: for an INT-pipe-bound generator
+        # (Threefry: ALU) report the pipe's utilisation from the committed ncu capture
+        n = per_gen[dom]["ncu"]
+        roofline["compute_roofline"] = {"pipe": n["binding_pipe"], "utilization_pct": n.get(n["binding_pipe"]),
+                                        "source": n["source"]}
 
     line = {"metric": METRIC, "value": round(value, 3), "unit": "Gsamples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,

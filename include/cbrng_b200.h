@@ -152,6 +152,30 @@ int cbrng_brownian_stats(uint64_t n, const uint64_t *pid, uint64_t pid_base, con
  * position-aware digest used to prove results are identical for any GPU count. */
 int cbrng_digest_u32(const uint32_t *words, uint64_t n, uint64_t global_offset, uint64_t *acc, void *stream);
 
+/* ---------------- statistical-battery producers ----------------
+ * Generators fused with the reductions of stats.py; counts are u64 [dev] and
+ * accumulated (+=), exact and order-independent. */
+/* byte histogram of n_words words of one stream (monobit / chi_square_bytes on
+ * run_battery's stream, stats.py:117-139, :300-306); same stream addressing and
+ * Tyche state convention as cbrng_words. counts: u64[256]. */
+int cbrng_stream_byte_histogram(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos,
+                                const uint32_t *tyche_state, uint64_t n_words, uint64_t *counts,
+                                uint32_t *tyche_state_out, void *stream);
+/* byte histogram of prefix_words(alg, seed_base + arange(n_streams), ctr, nwords), i.e. one
+ * iteration of iter_interleave_chunks (stats.py:276-286). */
+int cbrng_prefix_byte_histogram(int alg, uint64_t seed_base, uint32_t ctr, uint64_t n_streams, uint32_t nwords,
+                                uint64_t *counts, void *stream);
+/* byte histogram of n bytes at data [dev, 4-byte aligned] (monobit(data), stats.py:117). */
+int cbrng_buffer_byte_histogram(const uint8_t *data, uint64_t n, uint64_t *counts, void *stream);
+/* avalanche_stats (stats.py:171-192): out[0] += sum popcount(w0 ^ w1), out[1 + b] += trials whose
+ * bit b differs, w0/w1 = first word of (seeds[i], ctrs[i]) / (seeds[i] ^ flips[i], ctrs[i]). */
+int cbrng_avalanche(int alg, const uint64_t *seeds, const uint32_t *ctrs, const uint64_t *flips, uint64_t n,
+                    uint64_t *out, void *stream);
+/* Pearson sums for interstream_correlation (stats.py:205-246): partials[k*5 + (0..4)] =
+ * (sum a, sum b, sum a^2, sum b^2, sum ab) of block k; reduce blocks in order on the host. */
+int cbrng_pearson_partials(const double *a, const double *b, uint64_t n, uint32_t n_blocks, double *partials,
+                           void *stream);
+
 /* _kernels.fnv1a64 (_kernels.py:89-96): byte-serial by definition, host only. */
 uint64_t cbrng_fnv1a64(const uint8_t *data, uint64_t n, uint64_t h);
 

@@ -148,10 +148,9 @@ __device__ __forceinline__ void step_update(double &x, double &y, double &vx, do
     y = __dadd_rn(y, __dmul_rn(vy, a.dt));
 }
 
-// MINB: minimum resident CTAs per SM requested from ptxas (register cap). The
-// fused kernel is latency-bound on the Philox chain at 5 CTAs (44 registers,
-// ncu: issue 55 %, FMA-heavy 66 %); capping at 6 CTAs (40 registers) measured
-// slower (3.27e11 vs 3.40e11 p-steps/s), so 5 is the default.
+// MINB: minimum resident CTAs per SM requested from ptxas (register cap). 5 CTAs
+// (<= 51 registers) measured 3.40e11 p-steps/s; 6 CTAs (40 registers, small
+// spill) 3.27e11 (profiles/r1j_tune.md).
 template <int ALG, bool HI0, bool FOLD, int MINB>
 __global__ void __launch_bounds__(256, MINB) brownian_steps_kernel(const __grid_constant__ BrownArgs a) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -220,14 +219,6 @@ __global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint
     }
 }
 
-static int brownian_minb() {
-    static int v = [] {
-        const char *e = getenv("CBRNG_BROWNIAN_MINB");
-        return e && atoi(e) == 6 ? 6 : 5;  // 5 measured faster (profiles/r1j_tune.md)
-    }();
-    return v;
-}
-
 template <int ALG, bool HI0, bool FOLD, int MINB>
 static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
     auto k = brownian_steps_kernel<ALG, HI0, FOLD, MINB>;
@@ -247,12 +238,8 @@ static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
 
 template <int ALG, bool HI0, bool FOLD>
 static int launch_steps_k(BrownArgs a, int mode, cudaStream_t st) {
-    if constexpr (!HI0) {
-        return launch_steps_kb<ALG, HI0, FOLD, 1>(a, mode, st);  // 64-bit pids: 20 live round keys, no cap
-    } else {
-        if (brownian_minb() == 5) return launch_steps_kb<ALG, HI0, FOLD, 5>(a, mode, st);
-        return launch_steps_kb<ALG, HI0, FOLD, 6>(a, mode, st);
-    }
+    if constexpr (!HI0) return launch_steps_kb<ALG, HI0, FOLD, 1>(a, mode, st);  // 64-bit pids: 20 live keys, no cap
+    else return launch_steps_kb<ALG, HI0, FOLD, 5>(a, mode, st);
 }
 
 template <int ALG>

@@ -18,15 +18,11 @@
 
 #include "cbrng_internal.cuh"
 #include "cbrng_bm.cuh"
+#include "cbrng_stream.cuh"
 
 namespace cbrng {
 
 enum Out : int { OUT_U32 = 0, OUT_F32 = 1, OUT_F64 = 2, OUT_NORMAL = 3 };
-
-template <int ALG> struct StreamOf;
-template <> struct StreamOf<PHILOX> { using T = PhiloxStream; };
-template <> struct StreamOf<THREEFRY> { using T = ThreefryStream; };
-template <> struct StreamOf<SQUARES> { using T = SquaresStream; };
 
 template <int ALG>
 struct FillArgs {
@@ -39,34 +35,6 @@ struct FillArgs {
     void *out1;
     uint32_t m24;      // 1 << 24 at run time (u32_to_f32_mul)
 };
-
-// V selects a code variant per algorithm. Threefry: V = 0 compiler-scheduled;
-// V = 1: all round adds forced to IMAD + 10 of 40 rotations on the multiplier;
-// V = 2: all round adds forced to IMAD, rotations on the ALU;
-// V = 3: all round adds forced to IMAD + 6 rotations on the multiplier.
-template <int ALG, int V>
-__device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, uint32_t bc) {
-    if constexpr (ALG == PHILOX) return philox_stream_block(p, bc);
-    else if constexpr (V == 0) return threefry_stream_block<0, false>(p, bc);
-    else if constexpr (V == 1) return threefry_stream_block<10, true>(p, bc);
-    else if constexpr (V == 2) return threefry_stream_block<0, true>(p, bc);
-    else return threefry_stream_block<6, true>(p, bc);
-}
-
-template <int ALG, bool SKIP, int V = 0>
-__device__ __forceinline__ uint4 unit_words(const typename StreamOf<ALG>::T &p, uint32_t bc0, uint32_t skip, uint64_t u) {
-    if constexpr (ALG == SQUARES) {
-        // V == 1: the host proved the fill never wraps the 32-bit counter
-        return squares_stream_word4<V == 1>(p, bc0 + 4u * (uint32_t)u);
-    } else if constexpr (!SKIP) {
-        return block_at<ALG, V>(p, bc0 + (uint32_t)u);
-    } else {
-        uint4 a = block_at<ALG, V>(p, bc0 + (uint32_t)u), b = block_at<ALG, V>(p, bc0 + (uint32_t)u + 1);
-        if (skip == 1) return make_uint4(a.y, a.z, a.w, b.x);
-        if (skip == 2) return make_uint4(a.z, a.w, b.x, b.y);
-        return make_uint4(a.w, b.x, b.y, b.z);
-    }
-}
 
 // MULSHIFT: 0 = shift + FMUL, 1 = shift on the multiplier (ALU-bound kernels),
 // 2 = exponent arithmetic on the ALU (FMA-heavy-bound kernels).

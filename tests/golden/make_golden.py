@@ -185,6 +185,25 @@ def main() -> None:
     g["panel"] = {"pairs": [[s, c_] for s, c_ in _digest_runner.stream_panel()], "words": _digest_runner.WORDS,
                   "sha256": _digest_runner.panel_digest()}
 
+    # --- statistical battery (stats.py): SURVEY §8(f) rank 1
+    from cbrng import stats as st
+    g["battery_16MiB"] = {}
+    for a in ALGS:
+        reps = st.run_battery(Algorithm.from_name(a), 16 * 2**20)
+        g["battery_16MiB"][a] = [st.report_to_dict(r) for r in reps]
+    blob = make_generator("squares", 3, 1).words(100_003).astype("<u4").tobytes()[:400_010]
+    g["blob_tests"] = {"monobit": st.report_to_dict(st.monobit(blob)),
+                       "chi_square_bytes": st.report_to_dict(st.chi_square_bytes(blob)),
+                       "ks_uniform": st.report_to_dict(st.ks_uniform(distributions.words_to_unit_doubles(
+                           make_generator("threefry", 5, 0).words(20_000))))}
+    g["avalanche_20000"] = {}
+    for a in ALGS:
+        av = st.avalanche_stats(Algorithm.from_name(a), 20_000)
+        g["avalanche_20000"][a] = {"mean": av.mean_hamming, "rates": av.bit_flip_rates.tolist(), "z": av.z}
+    spec = st.InterleaveSpec(n_streams=1000, draws_per_stream=3, iterations=4)
+    g["interleave_1000x3x4"] = {a: sha(np.frombuffer(st.interleave_stream(spec, Algorithm.from_name(a), 77),
+                                                     dtype=np.uint8)) for a in ALGS}
+
     (OUT / "golden.json").write_text(json.dumps(g, indent=1, sort_keys=True) + "\n")
     np.savez_compressed(OUT / "golden.npz", **arrays)
     print("wrote", OUT / "golden.json", OUT / "golden.npz",

@@ -1,0 +1,80 @@
+"""§8(f) rank 1: the statistical battery's data producers fused on the GPU
+(cbrng_stream/prefix/buffer_byte_histogram, cbrng_avalanche,
+cbrng_pearson_partials) against the reference's own reports
+(tests/golden: run_battery, monobit/chi-square/KS on fixed blobs, avalanche,
+interleave digests) and the CPU oracle."""
+
+from __future__ import annotations
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from conftest import ALGS
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def st():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2310_19925_b200 import stats
+
+    return stats
+
+
+def test_histograms_exact(st, oracle):
+    for alg in ALGS:
+        for n in (1, 5, 4096, 100_003):
+            c = st.histogram_stream(alg, 9, 2, n).cpu().numpy()
+            ref = np.bincount(oracle.stream_words(alg, 9, 2, n).view(np.uint8), minlength=256)
+            assert np.array_equal(c, ref), (alg, n)
+    blob = np.random.default_rng(3).integers(0, 256, 100_007, dtype=np.uint8)
+    assert np.array_equal(st.histogram_bytes(blob).cpu().numpy(), np.bincount(blob, minlength=256))
+
+
+def test_interleave_histogram_matches_blob(st, oracle, golden):
+    spec = st.InterleaveSpec(n_streams=1000, draws_per_stream=3, iterations=4)
+    for alg in ALGS:
+        blob = st.interleave_stream(spec, alg, 77)
+        assert hashlib.sha256(blob).hexdigest() == golden["interleave_1000x3x4"][alg]
+        c = st.interleave_histogram(spec, alg, 77).cpu().numpy()
+        assert np.array_equal(c, np.bincount(np.frombuffer(blob, np.uint8), minlength=256))
+
+
+def test_blob_reports(st, oracle, golden):
+    blob = oracle.stream_words("squares", 3, 1, 100_003).astype("<u4").tobytes()[:400_010]
+    assert st.report_to_dict(st.monobit(blob)) == golden["blob_tests"]["monobit"]
+    assert st.report_to_dict(st.chi_square_bytes(blob)) == golden["blob_tests"]["chi_square_bytes"]
+    u = oracle.uniform_f64("threefry", 5, 0, 10_000)
+    assert st.report_to_dict(st.ks_uniform(u)) == golden["blob_tests"]["ks_uniform"]
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_avalanche_exact(st, golden, alg):
+    av = st.avalanche_stats(alg, 20_000)
+    ref = golden["avalanche_20000"][alg]
+    assert av.mean_hamming == ref["mean"] and av.z == ref["z"]
+    assert av.bit_flip_rates.tolist() == ref["rates"]
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_run_battery_matches_reference(st, golden, alg):
+    """Every report of the reference's 16 MiB battery: integer-count statistics
+    bit-identical; the correlation (sums vs numpy's two-pass corrcoef) to 1e-9."""
+    got = [st.report_to_dict(r) for r in st.run_battery(alg, 16 * 2**20)]
+    ref = golden["battery_16MiB"][alg]
+    assert [g["test_name"] for g in got] == [r["test_name"] for r in ref]
+    for g, r in zip(got, ref):
+        assert g["verdict"] == r["verdict"] and g["n_samples"] == r["n_samples"]
+        if g["test_name"] == "interstream_correlation":
+            assert math.isclose(g["statistic"], r["statistic"], rel_tol=1e-9)
+            assert math.isclose(g["p_value_or_z"], r["p_value_or_z"], rel_tol=1e-6)
+        else:
+            assert g == r, g["test_name"]
+    assert st.battery_passes(st.run_battery(alg, 16 * 2**20))

@@ -198,3 +198,40 @@ class TestFnv:
         assert oracle.fnv1a64(b"") == golden["fnv"]["empty"]
         assert oracle.fnv1a64(bytes(40)) == golden["fnv"]["zero40"]
         assert oracle.fnv1a64(bytes(range(256)) * 3) == golden["fnv"]["bytes0_255x3"]
+
+
+class TestBatteryHostFormulas:
+    """stats.py's statistic -> p-value -> verdict arithmetic, fed with byte
+    histograms of oracle-generated words, reproduces the reference's reports."""
+
+    def test_blob_reports(self, oracle, golden):
+        import numpy as np
+
+        from paper_2310_19925_b200 import stats as st
+
+        blob = oracle.stream_words("squares", 3, 1, 100_003).astype("<u4").tobytes()[:400_010]
+        counts = np.bincount(np.frombuffer(blob, np.uint8), minlength=256)
+        assert st.report_to_dict(st.monobit_from_counts(counts)) == golden["blob_tests"]["monobit"]
+        assert st.report_to_dict(st.chi_square_from_counts(counts)) == golden["blob_tests"]["chi_square_bytes"]
+
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_battery_stream_reports(self, oracle, golden, alg):
+        import numpy as np
+
+        from paper_2310_19925_b200 import stats as st
+
+        words = oracle.stream_words(alg, st.DEFAULT_BATTERY_SEED, 0, 16 * 2**20 // 4)
+        counts = np.bincount(words.view(np.uint8), minlength=256)
+        ref = golden["battery_16MiB"][alg]
+        assert st.report_to_dict(st.monobit_from_counts(counts)) == ref[0]
+        assert st.report_to_dict(st.chi_square_from_counts(counts)) == ref[1]
+
+    def test_classify_p_bands(self):
+        from paper_2310_19925_b200 import stats as st
+
+        assert st.classify_p(0.5) is st.Verdict.PASS
+        assert st.classify_p(1e-5) is st.Verdict.SUSPICIOUS
+        assert st.classify_p(1 - 1e-5) is st.Verdict.SUSPICIOUS
+        assert st.classify_p(1e-7) is st.Verdict.FAIL
+        assert st.classify_p(1 - 1e-7, folded=True) is st.Verdict.PASS
+        assert st.classify_p(float("nan")) is st.Verdict.FAIL
