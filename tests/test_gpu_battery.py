@@ -78,3 +78,30 @@ def test_run_battery_matches_reference(st, golden, alg):
         else:
             assert g == r, g["test_name"]
     assert st.battery_passes(st.run_battery(alg, 16 * 2**20))
+
+
+@pytest.mark.parametrize("alg", ALGS)
+def test_emit_words_and_bytes(st, oracle, alg):
+    """§8(f) rank 2: raw emission == the stream's little-endian words; state advanced."""
+    import io
+
+    import paper_2310_19925_b200 as cb
+    from paper_2310_19925_b200 import emit
+
+    n = (1 << 16) + 5 if alg != "tyche" else 20_000
+    g = cb.make_generator(alg, 5, 2)
+    buf = io.BytesIO()
+    assert emit.emit_words(g, n, buf, chunk_words=4099) == 4 * n
+    ref = oracle.stream_words(alg, 5, 2, n + 3)
+    assert buf.getvalue() == ref[:n].astype("<u4").tobytes()
+    assert g.next_u32() == int(ref[n])
+    g2 = cb.make_generator(alg, 5, 2)
+    b2 = io.BytesIO()
+    emit.emit_bytes(g2, 4 * n + 3, b2)
+    assert b2.getvalue() == cb.fill_bytes(cb.make_generator(alg, 5, 2), 4 * n + 3)
+
+
+def test_emit_cli_exit_codes(st):
+    from paper_2310_19925_b200 import emit
+
+    assert emit.main(["--gen", "nope", "--n", "4"]) == 2
