@@ -161,10 +161,10 @@ int cbrng_digest_u32(const uint32_t *words, uint64_t n, uint64_t global_offset, 
 int cbrng_stream_byte_histogram(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos,
                                 const uint32_t *tyche_state, uint64_t n_words, uint64_t *counts,
                                 uint32_t *tyche_state_out, void *stream);
-/* byte histogram of prefix_words(alg, seed_base + arange(n_streams), ctr, nwords), i.e. one
- * iteration of iter_interleave_chunks (stats.py:276-286). */
-int cbrng_prefix_byte_histogram(int alg, uint64_t seed_base, uint32_t ctr, uint64_t n_streams, uint32_t nwords,
-                                uint64_t *counts, void *stream);
+/* byte histogram of prefix_words(alg, seed_base + arange(n_streams), ctr0 + t, nwords) over
+ * t = 0..n_ctrs-1, i.e. n_ctrs iterations of iter_interleave_chunks (stats.py:276-286), one launch. */
+int cbrng_prefix_byte_histogram(int alg, uint64_t seed_base, uint32_t ctr0, uint32_t n_ctrs, uint64_t n_streams,
+                                uint32_t nwords, uint64_t *counts, void *stream);
 /* byte histogram of n bytes at data [dev, 4-byte aligned] (monobit(data), stats.py:117). */
 int cbrng_buffer_byte_histogram(const uint8_t *data, uint64_t n, uint64_t *counts, void *stream);
 /* avalanche_stats (stats.py:171-192): out[0] += sum popcount(w0 ^ w1), out[1 + b] += trials whose

@@ -54,7 +54,7 @@ SIGNATURES = {
     "cbrng_brownian_stats": (i32, [u64, vp, u64, vp, vp, vp, vp, vp, vp]),
     "cbrng_digest_u32": (i32, [vp, u64, u64, vp, vp]),
     "cbrng_stream_byte_histogram": (i32, [i32, u64, u32, u64, vp, u64, vp, vp, vp]),
-    "cbrng_prefix_byte_histogram": (i32, [i32, u64, u32, u64, u32, vp, vp]),
+    "cbrng_prefix_byte_histogram": (i32, [i32, u64, u32, u32, u64, u32, vp, vp]),
     "cbrng_buffer_byte_histogram": (i32, [vp, u64, vp, vp]),
     "cbrng_avalanche": (i32, [i32, vp, vp, vp, u64, vp, vp]),
     "cbrng_pearson_partials": (i32, [vp, vp, u64, u32, vp, vp]),

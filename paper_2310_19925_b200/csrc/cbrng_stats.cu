@@ -108,9 +108,10 @@ static int launch_stream_hist(uint64_t seed, uint32_t sc, uint64_t word_pos, uin
 // ---------------- many short streams (interleave) ----------------
 struct MultiHistArgs {
     uint64_t seed_base;
-    uint32_t ctr;
+    uint32_t ctr0;     // iteration t uses counter ctr0 + t
     uint32_t nwords;
     uint64_t n_streams;
+    uint64_t n_total;  // n_streams * n_iterations (stream, iteration) pairs
     unsigned long long *counts;
 };
 
@@ -146,9 +147,11 @@ __global__ void __launch_bounds__(ST_BLOCK) multi_hist_kernel(const __grid_const
     __shared__ uint32_t h[256];
     hist_init(h);
     const SmemHist H{h};
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_streams;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        for_stream_words<ALG>(a.seed_base + i, a.ctr, a.nwords, [&](uint32_t w) { H.add_word(w); });
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n_total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = i / a.n_streams, p = i - t * a.n_streams;
+        for_stream_words<ALG>(a.seed_base + p, a.ctr0 + (uint32_t)t, a.nwords, [&](uint32_t w) { H.add_word(w); });
+    }
     hist_flush(h, a.counts);
 }
 
@@ -251,15 +254,15 @@ int cbrng_stream_byte_histogram(int alg, uint64_t seed, uint32_t stream_ctr, uin
     }
 }
 
-int cbrng_prefix_byte_histogram(int alg, uint64_t seed_base, uint32_t ctr, uint64_t n_streams, uint32_t nwords,
-                                uint64_t *counts, void *stream) {
+int cbrng_prefix_byte_histogram(int alg, uint64_t seed_base, uint32_t ctr0, uint32_t n_ctrs, uint64_t n_streams,
+                                uint32_t nwords, uint64_t *counts, void *stream) {
     CBRNG_CHECK_ALG(alg);
     clear_error();
     CBRNG_REQUIRE(counts, "counts is NULL");
-    if (n_streams == 0 || nwords == 0) return CBRNG_OK;
-    MultiHistArgs a{seed_base, ctr, nwords, n_streams, reinterpret_cast<unsigned long long *>(counts)};
+    if (n_streams == 0 || nwords == 0 || n_ctrs == 0) return CBRNG_OK;
+    MultiHistArgs a{seed_base, ctr0, nwords, n_streams, n_streams * n_ctrs, reinterpret_cast<unsigned long long *>(counts)};
     cudaStream_t st = as_stream(stream);
-    const uint64_t work = (n_streams + ST_BLOCK - 1) / ST_BLOCK;
+    const uint64_t work = (a.n_total + ST_BLOCK - 1) / ST_BLOCK;
     switch (alg) {
         case PHILOX: { auto k = multi_hist_kernel<PHILOX>; k<<<grid_for(k, ST_BLOCK, 0, work), ST_BLOCK, 0, st>>>(a); break; }
         case THREEFRY: { auto k = multi_hist_kernel<THREEFRY>; k<<<grid_for(k, ST_BLOCK, 0, work), ST_BLOCK, 0, st>>>(a); break; }
