@@ -145,15 +145,70 @@ __global__ void __launch_bounds__(256) prefix_kernel(const __grid_constant__ Pre
 constexpr int TY_WARPS = 8;  // 256 threads
 constexpr int TY_CH = 4;     // staged 16-byte chunks per stream row = 16 words (64 B)
 
+// One stream walked word by word by one thread (the staged kernel below).
+// Counter-based algorithms fold the stream-only rounds once per row
+// (philox/threefry_stream_setup), so a 256-word row pays the setup once instead
+// of once per 4-word block; Tyche is serial anyway.
+template <int ALG> struct RowGen;
+template <> struct RowGen<PHILOX> {
+    PhiloxStream p;
+    uint32_t b = 0;
+    __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) : p(philox_stream_setup(seed, c)) {}
+    __device__ __forceinline__ uint4 next4() { return philox_stream_block(p, b++); }
+    __device__ __forceinline__ uint4 tail4() { return philox_stream_block(p, b); }
+};
+template <> struct RowGen<THREEFRY> {
+    ThreefryStream p;
+    uint32_t b = 0;
+    __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) : p(threefry_stream_setup(seed, c)) {}
+    __device__ __forceinline__ uint4 next4() { return threefry_stream_block<0, true>(p, b++); }
+    __device__ __forceinline__ uint4 tail4() { return threefry_stream_block<0, true>(p, b); }
+};
+template <> struct RowGen<SQUARES> {
+    SquaresStream p;
+    uint32_t j = 0;
+    __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) {
+        p.key = squares_key(seed);
+        p.base = ((uint64_t)c << 32) * p.key;
+    }
+    __device__ __forceinline__ uint4 next4() { uint4 w = squares_stream_word4<true>(p, j); j += 4; return w; }
+    __device__ __forceinline__ uint4 tail4() { return squares_stream_word4<true>(p, j); }
+};
+template <> struct RowGen<TYCHE> {
+    uint32_t A, B, C, D;
+    __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) {
+        const uint4 s = tyche_init(seed, c);
+        A = s.x; B = s.y; C = s.z; D = s.w;
+    }
+    __device__ __forceinline__ uint4 next4() {
+        uint4 w;
+        tyche_mix(A, B, C, D); w.x = B;
+        tyche_mix(A, B, C, D); w.y = B;
+        tyche_mix(A, B, C, D); w.z = B;
+        tyche_mix(A, B, C, D); w.w = B;
+        return w;
+    }
+    __device__ __forceinline__ uint4 tail4() { return next4(); }
+};
+
 // Staging slot of (row r, chunk c) in a warp's 32 x 4-chunk tile. The XOR
 // swizzle keeps both the row-wise STS.128 (lane = row) and the column-wise
 // LDS.128 (8 lanes = 2 rows x 4 chunks) conflict-free, without padding.
 __device__ __forceinline__ uint32_t ty_slot(uint32_t r, uint32_t c) { return r * TY_CH + (c ^ ((r >> 1) & 3)); }
 
-// VEC: rows are 16-byte aligned (nwords % 4 == 0) -> 128-bit stores. Both the
-// alignment case and the f32 map are compile-time so the copy-out is branch-free.
-template <int OUT, bool VEC>
-__global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_constant__ PrefixArgs a) {
+// One thread per stream; a warp transposes its 32 streams x 16 words through
+// shared memory so each global store instruction writes 8 rows x 64 B.
+// VEC: rows are 16-byte aligned (nwords % 4 == 0) -> 128-bit stores. MUL: the
+// f32 shift on the multiplier (ALU-bound generators). Compile-time so the
+// copy-out is branch-free.
+// Occupancy: Tyche's row state is 4 registers (32-register cap, 8 CTAs/SM);
+// the counter-based row generators keep the folded stream setup live (~20
+// registers for Philox: 4 CTAs/SM, <= 64 registers, spill-free), the others 5.
+template <int ALG> constexpr int staged_min_blocks() { return ALG == TYCHE ? 8 : (ALG == PHILOX ? 4 : 5); }
+
+template <int ALG, int OUT, bool VEC>
+__global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_kernel(const __grid_constant__ PrefixArgs a) {
+    constexpr bool MUL = ALG == TYCHE || ALG == THREEFRY;
     __shared__ uint4 tile[TY_WARPS][32 * TY_CH];  // 16 KB per CTA: 8 CTAs (64 warps) fit an SM
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -169,29 +224,21 @@ __global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_const
     for (uint64_t s0 = warp * 32; s0 < a.n_streams; s0 += nwarps * 32) {
         const uint64_t sid = s0 + lane;
         const bool valid = sid < a.n_streams;
-        uint4 st = tyche_init(valid ? seed_of(a, sid) : 0, valid ? ctr_of(a, sid) : 0);
-        uint32_t A = st.x, B = st.y, C = st.z, D = st.w;
+        RowGen<ALG> gen(valid ? seed_of(a, sid) : 0, valid ? ctr_of(a, sid) : 0);
         // output word index of (row rrow + 8k, chunk rc) in group g: obase + k*rstride + 16g
         uint64_t at = (s0 + rrow) * a.nwords + rc * 4;
         const uint64_t rstride = 8ull * a.nwords;
         const uint32_t rows_left = a.n_streams - s0 < 32 ? (uint32_t)(a.n_streams - s0) : 32u;
         for (uint32_t g = 0; g < groups; g++, at += 16) {
 #pragma unroll
-            for (int c = 0; c < TY_CH; c++) {
-                uint4 w;
-                tyche_mix(A, B, C, D); w.x = B;
-                tyche_mix(A, B, C, D); w.y = B;
-                tyche_mix(A, B, C, D); w.z = B;
-                tyche_mix(A, B, C, D); w.w = B;
-                my[lane * TY_CH + (c ^ wx)] = w;
-            }
+            for (int c = 0; c < TY_CH; c++) my[lane * TY_CH + (c ^ wx)] = gen.next4();
             __syncwarp();
 #pragma unroll
             for (int k = 0; k < 4; k++) {
                 if (rrow + 8 * k < rows_left) {
                     const uint4 v = my[rslot + 32 * k];
                     if constexpr (VEC) {
-                        store4<OUT, true>(a.out, at + k * rstride, v, a.m24);  // ALU-bound: shift on the multiplier
+                        store4<OUT, MUL>(a.out, at + k * rstride, v, a.m24);
                     } else {  // rows not 16-byte aligned (nwords % 4 != 0)
                         const uint64_t o = at + k * rstride;
                         store1<OUT>(a.out, o, v.x); store1<OUT>(a.out, o + 1, v.y);
@@ -201,25 +248,48 @@ __global__ void __launch_bounds__(256, 8) tyche_prefix_kernel(const __grid_const
             }
             __syncwarp();
         }
-        for (uint32_t j = 0; j < rem; j++) {
-            tyche_mix(A, B, C, D);
-            if (valid) store1<OUT>(a.out, sid * a.nwords + groups * 16 + j, B);
+        for (uint32_t j = 0; j < rem; j += 4) {
+            const uint4 w = gen.tail4();
+            gen.next4();  // advance (Tyche: tail4 already advanced; harmless past the row end)
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+            if (valid)
+                for (uint32_t q = 0; q < 4 && j + q < rem; q++) store1<OUT>(a.out, sid * a.nwords + groups * 16 + j + q, ws[q]);
         }
     }
 }
 
 template <int ALG, int OUT>
-static int launch_prefix(const PrefixArgs &a, cudaStream_t st) {
+static int launch_staged(const PrefixArgs &a, cudaStream_t st) {
     if (a.nwords % 4 == 0) {
-        auto k = prefix_kernel<ALG, OUT, 4>;
-        uint64_t chunks = a.n_streams * (a.nwords / 4);
-        k<<<grid_for(k, 256, 0, (chunks + 255) / 256), 256, 0, st>>>(a);
+        auto k = staged_prefix_kernel<ALG, OUT, true>;
+        k<<<grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
     } else {
-        auto k = prefix_kernel<ALG, OUT, 1>;
-        uint64_t chunks = a.n_streams * a.nwords;
-        k<<<grid_for(k, 256, 0, (chunks + 255) / 256), 256, 0, st>>>(a);
+        auto k = staged_prefix_kernel<ALG, OUT, false>;
+        k<<<grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
     }
-    return check_launch("prefix_kernel");
+    return check_launch("staged_prefix_kernel");
+}
+
+template <int ALG, int OUT>
+static int launch_prefix(const PrefixArgs &a, cudaStream_t st) {
+    // Rows of >= 16 words: one thread per stream with the stream setup folded
+    // once per row, staged through shared memory (ncu: the warp-per-row kernel
+    // spends ~20 % of its FMA-heavy cycles re-deriving the key schedule).
+    if constexpr (ALG == TYCHE) {
+        return launch_staged<ALG, OUT>(a, st);
+    } else {
+        if (a.nwords >= 16) return launch_staged<ALG, OUT>(a, st);
+        if (a.nwords % 4 == 0) {
+            auto k = prefix_kernel<ALG, OUT, 4>;
+            uint64_t chunks = a.n_streams * (a.nwords / 4);
+            k<<<grid_for(k, 256, 0, (chunks + 255) / 256), 256, 0, st>>>(a);
+        } else {
+            auto k = prefix_kernel<ALG, OUT, 1>;
+            uint64_t chunks = a.n_streams * a.nwords;
+            k<<<grid_for(k, 256, 0, (chunks + 255) / 256), 256, 0, st>>>(a);
+        }
+        return check_launch("prefix_kernel");
+    }
 }
 
 template <int OUT>
@@ -233,27 +303,13 @@ static int dispatch_prefix(int alg, const uint64_t *seeds, uint64_t seed_base, c
         set_error("output pointer not 16-byte aligned");
         return CBRNG_EALIGN;
     }
-    PrefixArgs a{seeds, seed_base, ctrs, ctr_scalar, nwords, n_streams, out, 0};
-    if (alg == TYCHE) a.m24 = 1u << 24;
+    PrefixArgs a{seeds, seed_base, ctrs, ctr_scalar, nwords, n_streams, out, 1u << 24};
     cudaStream_t st = as_stream(stream);
     switch (alg) {
         case PHILOX: return launch_prefix<PHILOX, OUT>(a, st);
         case THREEFRY: return launch_prefix<THREEFRY, OUT>(a, st);
         case SQUARES: return launch_prefix<SQUARES, OUT>(a, st);
-        default: {
-            if (nwords >= 16 && nwords % 4 == 0 && !aligned(out, 16)) {
-                set_error("output pointer not 16-byte aligned");
-                return CBRNG_EALIGN;
-            }
-            if (nwords % 4 == 0) {
-                auto k = tyche_prefix_kernel<OUT, true>;
-                k<<<grid_for(k, 256, 0, (n_streams + 255) / 256), 256, 0, st>>>(a);
-            } else {
-                auto k = tyche_prefix_kernel<OUT, false>;
-                k<<<grid_for(k, 256, 0, (n_streams + 255) / 256), 256, 0, st>>>(a);
-            }
-            return check_launch("tyche_prefix_kernel");
-        }
+        default: return launch_prefix<TYCHE, OUT>(a, st);
     }
 }
 
