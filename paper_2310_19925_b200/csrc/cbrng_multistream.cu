@@ -155,14 +155,12 @@ template <> struct RowGen<PHILOX> {
     uint32_t b = 0;
     __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) : p(philox_stream_setup(seed, c)) {}
     __device__ __forceinline__ uint4 next4() { return philox_stream_block(p, b++); }
-    __device__ __forceinline__ uint4 tail4() { return philox_stream_block(p, b); }
 };
 template <> struct RowGen<THREEFRY> {
     ThreefryStream p;
     uint32_t b = 0;
     __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) : p(threefry_stream_setup(seed, c)) {}
     __device__ __forceinline__ uint4 next4() { return threefry_stream_block<0, true>(p, b++); }
-    __device__ __forceinline__ uint4 tail4() { return threefry_stream_block<0, true>(p, b); }
 };
 template <> struct RowGen<SQUARES> {
     SquaresStream p;
@@ -172,7 +170,6 @@ template <> struct RowGen<SQUARES> {
         p.base = ((uint64_t)c << 32) * p.key;
     }
     __device__ __forceinline__ uint4 next4() { uint4 w = squares_stream_word4<true>(p, j); j += 4; return w; }
-    __device__ __forceinline__ uint4 tail4() { return squares_stream_word4<true>(p, j); }
 };
 template <> struct RowGen<TYCHE> {
     uint32_t A, B, C, D;
@@ -188,7 +185,6 @@ template <> struct RowGen<TYCHE> {
         tyche_mix(A, B, C, D); w.w = B;
         return w;
     }
-    __device__ __forceinline__ uint4 tail4() { return next4(); }
 };
 
 // Staging slot of (row r, chunk c) in a warp's 32 x 4-chunk tile. The XOR
@@ -249,8 +245,7 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_k
             __syncwarp();
         }
         for (uint32_t j = 0; j < rem; j += 4) {
-            const uint4 w = gen.tail4();
-            gen.next4();  // advance (Tyche: tail4 already advanced; harmless past the row end)
+            const uint4 w = gen.next4();  // may run up to 3 words past the row end: discarded
             const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
             if (valid)
                 for (uint32_t q = 0; q < 4 && j + q < rem; q++) store1<OUT>(a.out, sid * a.nwords + groups * 16 + j + q, ws[q]);
