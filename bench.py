@@ -264,7 +264,7 @@ def main() -> None:
             # the INT-pipe side of the roofline, from the committed ncu capture:
             # the busiest of issue / ALU / FMA-heavy is the kernel's compute bound
             pats = {"philox": "fill_kernel<0, 1", "threefry": "fill_kernel<1, 1", "squares": "fill_kernel<2, 1",
-                    "tyche": "tyche_prefix_kernel<1>"}
+                    "tyche": "staged_prefix_kernel<3, 1"}
             for a, pat in pats.items():
                 k = next((k for k in summ.get("kernels", []) if pat in k["kernel"]), None)
                 if k:

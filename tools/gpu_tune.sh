@@ -1,4 +1,2 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-TUNE_GRID=8 TUNE_ILP=4 TUNE_TF=2 timeout 900 python tools/tune_fills.py > gpurun_out/tune.log 2>&1
-timeout 600 python tools/bench_next.py > gpurun_out/bench_next.json 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fill_kernel|brownian_steps|staged_prefix" -c 3 -o gpurun_out/prof_bm2 python tools/prof_kernels.py normal brownian prefix > gpurun_out/ncu_full.log 2>&1

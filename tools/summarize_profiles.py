@@ -112,7 +112,8 @@ def main() -> None:
                 + ", ".join(f"{k} {v:.1f}" for k, v in d["top_stalls"].items()) + " |")
         (PROF / f"{tag}_ncu.md").write_text("\n".join(lines) + "\n")
         names = {"fill_kernel<0, 1": "uniform_f32_philox", "fill_kernel<1, 1": "uniform_f32_threefry",
-                 "fill_kernel<2, 1": "uniform_f32_squares", "tyche_prefix_kernel<1>": "uniform_f32_tyche"}
+                 "fill_kernel<2, 1": "uniform_f32_squares", "staged_prefix_kernel<3, 1": "uniform_f32_tyche",
+                 "tyche_prefix_kernel<1": "uniform_f32_tyche"}
         traffic = {}
         for d in ks:
             for pat, nm in names.items():
