@@ -106,8 +106,16 @@ def as_dev(x, np_dtype, device=None) -> torch.Tensor:
     """Contiguous CUDA tensor of dtype np_dtype from numpy / python / torch input."""
     tdt = TORCH_OF[np.dtype(np_dtype)]
     if isinstance(x, torch.Tensor):
+        dev = cuda_device(device if device is not None else (x.device if x.is_cuda else None))
         if x.dtype != tdt:
-            x = x.to(torch.int64).to(tdt) if x.dtype.is_floating_point is False else x.to(tdt)
-        return x.to(cuda_device(device if device is not None else (x.device if x.is_cuda else None))).contiguous()
+            same_width_ints = (not x.dtype.is_floating_point and not tdt.is_floating_point
+                               and x.element_size() == np.dtype(np_dtype).itemsize)
+            if same_width_ints:
+                x = x.contiguous().view(tdt)  # two's-complement reinterpretation, as numpy's astype
+            elif x.dtype.is_floating_point and tdt.is_floating_point:
+                x = x.to(tdt)
+            else:  # integer width changes: numpy's wrapping conversion on the host
+                x = torch.from_numpy(np.ascontiguousarray(x.detach().cpu().numpy().astype(np_dtype)))
+        return x.to(dev).contiguous()
     a = np.ascontiguousarray(np.asarray(x).astype(np_dtype, copy=False))
     return torch.from_numpy(a).to(cuda_device(device))

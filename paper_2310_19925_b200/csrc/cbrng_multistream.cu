@@ -3,15 +3,13 @@
 // (bulk.py:49-159).
 //
 // Output is row-major out[stream][word] exactly as the reference returns it.
-// Counter-based algorithms (Philox/Threefry/Squares) are random access in both
-// axes, so lanes are mapped to contiguous 16-byte chunks of the output:
-//   * rows of >= 128 words: one warp per row, lane l takes chunks l, l+32, ...
-//     (the per-stream key schedule is hoisted out of the chunk loop);
-//   * shorter rows: a warp covers floor(32 / chunks_per_row) whole rows per pass.
-// Either way each warp store instruction writes one contiguous run.
-// Tyche is serial within a stream (bulk.py:9-11): one thread per stream, and a
-// warp transposes its 32 streams x 32 words through padded shared memory so the
-// global stores are full 128-byte lines.
+//   * rows of >= 16 words (and every Tyche row: serial within a stream,
+//     bulk.py:9-11): one thread per stream walks its row with the stream-only
+//     cipher setup folded once per row; a warp transposes its 32 streams x 16
+//     words through swizzled shared memory, so each store instruction writes
+//     8 rows x 64 contiguous bytes (staged_prefix_kernel);
+//   * shorter rows: lanes map to contiguous 16-byte chunks of consecutive rows
+//     (prefix_kernel).
 #include "cbrng_internal.cuh"
 
 namespace cbrng {
@@ -56,26 +54,6 @@ template <> struct StreamKey<SQUARES> {
     __device__ __forceinline__ uint4 block(uint32_t b) const { return squares_stream_word4(p, 4 * b); }
 };
 
-// Long rows (>= 128 words): a warp owns one stream, so the stream-only part of
-// the cipher (round keys, Philox rounds 0-3 / Threefry rounds 0-1) is folded
-// once per row and amortised over the row's blocks (philox_stream_setup is the
-// same fold the single-stream fills do on the host).
-template <int ALG> struct RowKey { using T = StreamKey<ALG>; };
-template <> struct RowKey<PHILOX> {
-    struct T {
-        PhiloxStream p;
-        __device__ __forceinline__ T(uint64_t seed, uint32_t c) : p(philox_stream_setup(seed, c)) {}
-        __device__ __forceinline__ uint4 block(uint32_t b) const { return philox_stream_block(p, b); }
-    };
-};
-template <> struct RowKey<THREEFRY> {
-    struct T {
-        ThreefryStream p;
-        __device__ __forceinline__ T(uint64_t seed, uint32_t c) : p(threefry_stream_setup(seed, c)) {}
-        __device__ __forceinline__ uint4 block(uint32_t b) const { return threefry_stream_block<0, false>(p, b); }
-    };
-};
-
 template <int ALG>
 __device__ __forceinline__ uint32_t single_word(const StreamKey<ALG> &k, uint32_t j) {
     if constexpr (ALG == SQUARES) {
@@ -110,35 +88,25 @@ __device__ __forceinline__ void store1(void *out, uint64_t word_index, uint32_t 
     else reinterpret_cast<float *>(out)[word_index] = u32_to_f32(w);
 }
 
-// CW = words per chunk: 4 (nwords % 4 == 0, 16-byte stores) or 1 (generic).
+// Short rows (< 16 words: Brownian init's 8, first_words' 1, ...): a warp covers
+// floor(32 / chunks_per_row) whole rows per pass, lane -> (row, chunk), so the
+// warp's stores are one contiguous run. CW = words per chunk: 4 (nwords % 4 == 0,
+// 16-byte stores) or 1 (generic). Longer rows take staged_prefix_kernel.
 template <int ALG, int OUT, int CW>
 __global__ void __launch_bounds__(256) prefix_kernel(const __grid_constant__ PrefixArgs a) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t cpr = a.nwords / CW;  // chunks per row
-    if (cpr >= 32) {
-        for (uint64_t row = warp; row < a.n_streams; row += nwarps) {
-            const uint64_t rbase = row * a.nwords;
-            if constexpr (CW == 4) {
-                const typename RowKey<ALG>::T k(seed_of(a, row), ctr_of(a, row));
-                for (uint32_t j = lane; j < cpr; j += 32) store4<OUT>(a.out, rbase + 4ull * j, k.block(j));
-            } else {
-                const StreamKey<ALG> k(seed_of(a, row), ctr_of(a, row));
-                for (uint32_t j = lane; j < cpr; j += 32) store1<OUT>(a.out, rbase + j, single_word<ALG>(k, j));
-            }
-        }
-    } else {
-        const uint32_t rpp = 32 / cpr;  // rows per pass
-        const uint32_t roff = lane / cpr, ch = lane - roff * cpr;
-        if (roff >= rpp) return;
-        for (uint64_t r0 = warp * rpp; r0 < a.n_streams; r0 += nwarps * rpp) {
-            const uint64_t row = r0 + roff;
-            if (row >= a.n_streams) break;
-            const StreamKey<ALG> k(seed_of(a, row), ctr_of(a, row));
-            if constexpr (CW == 4) store4<OUT>(a.out, row * a.nwords + 4ull * ch, k.block(ch));
-            else store1<OUT>(a.out, row * a.nwords + ch, single_word<ALG>(k, ch));
-        }
+    const uint32_t cpr = a.nwords / CW;  // chunks per row, < 32 here
+    const uint32_t rpp = 32 / cpr;       // rows per pass
+    const uint32_t roff = lane / cpr, ch = lane - roff * cpr;
+    if (roff >= rpp) return;
+    for (uint64_t r0 = warp * rpp; r0 < a.n_streams; r0 += nwarps * rpp) {
+        const uint64_t row = r0 + roff;
+        if (row >= a.n_streams) break;
+        const StreamKey<ALG> k(seed_of(a, row), ctr_of(a, row));
+        if constexpr (CW == 4) store4<OUT>(a.out, row * a.nwords + 4ull * ch, k.block(ch));
+        else store1<OUT>(a.out, row * a.nwords + ch, single_word<ALG>(k, ch));
     }
 }
 
