@@ -151,7 +151,7 @@ static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
 
 // Units per thread per tile (independent cipher chains in flight per thread).
 // Defaults from the B200 sweeps in profiles/r1{c,d}_tune.md: 4 for every
-// algorithm. CBRNG_FILL_ILP=1|2|4 overrides for tuning runs.
+// algorithm. CBRNG_FILL_ILP=1|2|4|8 overrides for tuning runs.
 template <int ALG, int OUT>
 static int fill_ilp() {
     static int v = [] {
@@ -160,7 +160,7 @@ static int fill_ilp() {
         // (ncu r1e at one pair: issue 64 %, "wait" the top stall).
         const int dflt = OUT == OUT_NORMAL ? 2 : 4;
         int x = e ? atoi(e) : dflt;
-        return (x == 1 || x == 2 || x == 4) ? x : dflt;
+        return (x == 1 || x == 2 || x == 4 || x == 8) ? x : dflt;
     }();
     return v;
 }
@@ -180,6 +180,7 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
     switch (fill_ilp<ALG, OUT>()) {
         case 1: return launch_fill_ilp<ALG, OUT, SKIP, 1, V>(a, st);
         case 4: return launch_fill_ilp<ALG, OUT, SKIP, 4, V>(a, st);
+        case 8: return launch_fill_ilp<ALG, OUT, SKIP, 8, V>(a, st);
         default: return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);
     }
 }
