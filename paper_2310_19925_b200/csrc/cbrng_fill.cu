@@ -150,17 +150,18 @@ static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
 }
 
 // Units per thread per tile (independent cipher chains in flight per thread).
-// Defaults from the B200 sweeps in profiles/r1{c,d}_tune.md: 4 for every
-// algorithm. CBRNG_FILL_ILP=1|2|4|8 overrides for tuning runs.
+// Default 8 for every algorithm and output (B200 sweep, profiles/r1o_tune.md:
+// Philox 6411 -> 6575 GB/s, Squares 4329 -> 4416, Box-Muller 2526 -> 2655 from
+// 4 to 8). CBRNG_FILL_ILP=1|2|4|8|16 overrides for tuning runs.
 template <int ALG, int OUT>
 static int fill_ilp() {
     static int v = [] {
         const char *e = getenv("CBRNG_FILL_ILP");
-        // Box-Muller: two pairs per thread hide the long FP64 dependency chains
-        // (ncu r1e at one pair: issue 64 %, "wait" the top stall).
-        const int dflt = OUT == OUT_NORMAL ? 2 : 4;
+        // Box-Muller included: more pairs per thread hide the long FP64
+        // dependency chains (ncu r1e at one pair: issue 64 %, "wait" the top stall).
+        const int dflt = 8;
         int x = e ? atoi(e) : dflt;
-        return (x == 1 || x == 2 || x == 4 || x == 8) ? x : dflt;
+        return (x == 1 || x == 2 || x == 4 || x == 8 || x == 16) ? x : dflt;
     }();
     return v;
 }
@@ -177,11 +178,18 @@ static int tf_variant() {
 
 template <int ALG, int OUT, bool SKIP, int V>
 static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
-    switch (fill_ilp<ALG, OUT>()) {
-        case 1: return launch_fill_ilp<ALG, OUT, SKIP, 1, V>(a, st);
-        case 4: return launch_fill_ilp<ALG, OUT, SKIP, 4, V>(a, st);
-        case 8: return launch_fill_ilp<ALG, OUT, SKIP, 8, V>(a, st);
-        default: return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);
+    if constexpr (SKIP) {
+        return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);  // resumed mid-block: rare, 2 blocks per unit
+    } else {
+        switch (fill_ilp<ALG, OUT>()) {
+            case 1: return launch_fill_ilp<ALG, OUT, SKIP, 1, V>(a, st);
+            case 2: return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);
+            case 4: return launch_fill_ilp<ALG, OUT, SKIP, 4, V>(a, st);
+            case 16:
+                if constexpr (OUT == OUT_U32 || OUT == OUT_F32) return launch_fill_ilp<ALG, OUT, SKIP, 16, V>(a, st);
+                else return launch_fill_ilp<ALG, OUT, SKIP, 8, V>(a, st);  // 16 spills for the FP64 maps
+            default: return launch_fill_ilp<ALG, OUT, SKIP, 8, V>(a, st);
+        }
     }
 }
 
@@ -192,14 +200,16 @@ static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
         if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) return launch_fill_v<ALG, OUT, SKIP, 1>(a, st);
         return launch_fill_v<ALG, OUT, SKIP, 0>(a, st);
     }
-    if constexpr (ALG == THREEFRY) {
+    if constexpr (ALG == THREEFRY && (OUT == OUT_U32 || OUT == OUT_F32)) {
         switch (tf_variant()) {
+            case 0: return launch_fill_v<ALG, OUT, SKIP, 0>(a, st);
             case 1: return launch_fill_v<ALG, OUT, SKIP, 1>(a, st);
             case 2: return launch_fill_v<ALG, OUT, SKIP, 2>(a, st);
             case 3: return launch_fill_v<ALG, OUT, SKIP, 3>(a, st);
             default: break;
         }
     }
+    if constexpr (ALG == THREEFRY) return launch_fill_v<ALG, OUT, SKIP, 2>(a, st);
     return launch_fill_v<ALG, OUT, SKIP, 0>(a, st);
 }
 
