@@ -147,6 +147,17 @@ int cbrng_brownian_stats(uint64_t n, const uint64_t *pid, uint64_t pid_base, con
                          const double *y, const double *vx, const double *vy, int64_t *acc,
                          void *stream);
 
+/* Snapshot / checksum records (brownian.py:198-250): n pid-ordered 40-byte `<Qdddd`
+ * records (pid u64, x, y, vx, vy f64, little-endian) packed from / unpacked to the SoA
+ * arrays, all [dev]; rec must be 8-byte aligned. unpack: pid may be NULL (dropped). */
+int cbrng_pack_records(uint64_t n, const uint64_t *pid, uint64_t pid_base, const double *x, const double *y,
+                       const double *vx, const double *vy, uint8_t *rec, void *stream);
+int cbrng_unpack_records(uint64_t n, const uint8_t *rec, uint64_t *pid, double *x, double *y, double *vx,
+                         double *vy, void *stream);
+/* *bad [dev, u32] is set to 1 if pid[0..n) is not strictly increasing (checksum
+ * precondition, brownian.py:209-212); it is never cleared. */
+int cbrng_pid_order_check(uint64_t n, const uint64_t *pid, uint32_t *bad, void *stream);
+
 /* ---------------- invariance digest ----------------
  * acc[dev, u64] += sum_i mix64(global_offset + i, words[i]) mod 2^64: an order-free,
  * position-aware digest used to prove results are identical for any GPU count. */

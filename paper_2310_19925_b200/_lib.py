@@ -53,6 +53,9 @@ SIGNATURES = {
     "cbrng_brownian_steps": (i32, [i32, u64, vp, u64, vp, vp, vp, vp, u32, u64, u64, f64, f64, f64, i32, vp]),
     "cbrng_brownian_stats": (i32, [u64, vp, u64, vp, vp, vp, vp, vp, vp]),
     "cbrng_digest_u32": (i32, [vp, u64, u64, vp, vp]),
+    "cbrng_pack_records": (i32, [u64, vp, u64, vp, vp, vp, vp, vp, vp]),
+    "cbrng_unpack_records": (i32, [u64, vp, vp, vp, vp, vp, vp, vp]),
+    "cbrng_pid_order_check": (i32, [u64, vp, vp, vp]),
     "cbrng_stream_byte_histogram": (i32, [i32, u64, u32, u64, vp, u64, vp, vp, vp]),
     "cbrng_prefix_byte_histogram": (i32, [i32, u64, u32, u32, u64, u32, vp, vp]),
     "cbrng_buffer_byte_histogram": (i32, [vp, u64, vp, vp]),

@@ -184,21 +184,30 @@ def run_sim(cfg: SimConfig, particles: Particles | None = None, start_iteration:
 
 
 def _packed_records(particles: Particles) -> np.ndarray:
-    h = particles.host()
-    cols = np.column_stack([h["pid"].astype("<u8"), h["x"].astype("<f8").view("<u8"), h["y"].astype("<f8").view("<u8"),
-                            h["vx"].astype("<f8").view("<u8"), h["vy"].astype("<f8").view("<u8")])
-    return np.ascontiguousarray(cols).view(np.uint8).ravel()
+    """The pid-ordered `<Qdddd` records as host bytes: packed on the device from
+    the SoA arrays (cbrng_pack_records), then one D2H copy into pinned memory."""
+    n = particles.n
+    rec = torch.empty(n * _RECORD.size, dtype=torch.uint8, device=particles.x.device)
+    pid_p, base, x, y, vx, vy = particles._ptrs()
+    _lib.check(_lib.lib().cbrng_pack_records(n, pid_p, base, x, y, vx, vy, rec.data_ptr(), _dev.sptr(particles.x)),
+               "pack_records")
+    h = torch.empty(rec.numel(), dtype=torch.uint8, pin_memory=True)
+    h.copy_(rec, non_blocking=True)
+    torch.cuda.current_stream(rec.device).synchronize()
+    return h.numpy()
 
 
 def checksum(particles: Particles) -> TrajectoryChecksum:
     """FNV-1a 64 over pid-ordered 40-byte records (brownian.py:209-223).
 
     FNV is byte-serial by definition (_kernels.py:89-96): the records are
-    copied to the host and folded by cbrng_fnv1a64 (native code in the library).
+    packed on the device, copied to the host and folded there by cbrng_fnv1a64.
     """
     if particles.pid is not None and particles.n > 1:
-        pid = particles.pid_array().astype(np.int64)
-        if np.any(np.diff(pid) <= 0):
+        bad = torch.zeros(1, dtype=torch.int32, device=particles.x.device)
+        _lib.check(_lib.lib().cbrng_pid_order_check(particles.n, particles.pid.data_ptr(), bad.data_ptr(),
+                                                    _dev.sptr(particles.x)), "pid_order_check")
+        if int(bad.item()):
             raise ValueError("particles must be sorted by pid")
     if particles.n == 0:
         return TrajectoryChecksum(FNV_OFFSET_BASIS)
@@ -242,11 +251,13 @@ def load_snapshot(path, device=None) -> tuple[Particles, int]:
         raw = np.frombuffer(fh.read(n * _RECORD.size), dtype=np.uint8)
     if raw.size != n * _RECORD.size:
         raise ValueError("truncated snapshot file")
-    rec = raw.view("<u8").reshape(n, 5)
     dev = _dev.cuda_device(device)
-    col = lambda k: torch.from_numpy(rec[:, k].copy().view("<f8")).to(dev)  # noqa: E731
-    pid = torch.from_numpy(rec[:, 0].copy()).to(dev)
-    return Particles(pid, col(1), col(2), col(3), col(4)), next_iteration
+    rec = torch.from_numpy(raw.copy()).to(dev)
+    pid = torch.empty(n, dtype=torch.uint64, device=dev)
+    x, y, vx, vy = (torch.empty(n, dtype=torch.float64, device=dev) for _ in range(4))
+    _lib.check(_lib.lib().cbrng_unpack_records(n, rec.data_ptr(), pid.data_ptr(), x.data_ptr(), y.data_ptr(),
+                                               vx.data_ptr(), vy.data_ptr(), _dev.sptr(rec)), "unpack_records")
+    return Particles(pid, x, y, vx, vy), next_iteration
 
 
 def write_run_report(path, cfg: SimConfig, result: SimResult) -> None:

@@ -258,6 +258,42 @@ static int launch_steps(BrownArgs a, int mode, cudaStream_t st) {
 
 using namespace cbrng;
 
+// Snapshot / checksum records (brownian.py:198-250): pid-ordered 40-byte
+// little-endian `<Qdddd` records, packed from the SoA arrays in HBM so only the
+// packed bytes cross PCIe. Each record is five 8-byte words; thread i writes
+// record i (a warp's 32 records are 1280 contiguous bytes, merged in L2).
+__global__ void __launch_bounds__(256) pack_records_kernel(uint64_t n, const uint64_t *pid, uint64_t pid_base,
+                                                           const double *x, const double *y, const double *vx,
+                                                           const double *vy, uint64_t *rec) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t *r = rec + 5 * i;
+        __stcs(r + 0, (unsigned long long)(pid ? pid[i] : pid_base + i));
+        __stcs(r + 1, (unsigned long long)__double_as_longlong(x[i]));
+        __stcs(r + 2, (unsigned long long)__double_as_longlong(y[i]));
+        __stcs(r + 3, (unsigned long long)__double_as_longlong(vx[i]));
+        __stcs(r + 4, (unsigned long long)__double_as_longlong(vy[i]));
+    }
+}
+
+// Inverse of pack_records_kernel (load_snapshot, brownian.py:233-250); pid may be NULL.
+__global__ void __launch_bounds__(256) unpack_records_kernel(uint64_t n, const uint64_t *rec, uint64_t *pid, double *x,
+                                                             double *y, double *vx, double *vy) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t *r = rec + 5 * i;
+        if (pid) pid[i] = __ldcs((const unsigned long long *)r);
+        x[i] = __longlong_as_double((long long)__ldcs((const unsigned long long *)r + 1));
+        y[i] = __longlong_as_double((long long)__ldcs((const unsigned long long *)r + 2));
+        vx[i] = __longlong_as_double((long long)__ldcs((const unsigned long long *)r + 3));
+        vy[i] = __longlong_as_double((long long)__ldcs((const unsigned long long *)r + 4));
+    }
+}
+
+// Nonzero flag if pid[] is not strictly increasing (checksum precondition, brownian.py:209-212).
+__global__ void __launch_bounds__(256) pid_order_kernel(uint64_t n, const uint64_t *pid, uint32_t *bad) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        if (pid[i] <= pid[i - 1]) *bad = 1u;
+}
+
 extern "C" {
 
 int cbrng_brownian_init(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_base, uint32_t init_ctr, double *x,
@@ -319,6 +355,39 @@ int cbrng_digest_u32(const uint32_t *words, uint64_t n, uint64_t global_offset, 
     auto k = digest_u32_kernel;
     k<<<grid_for(k, 256, 0, (n + 255) / 256), 256, 0, as_stream(stream)>>>(words, n, global_offset, acc);
     return check_launch("digest_u32_kernel");
+}
+
+int cbrng_pack_records(uint64_t n, const uint64_t *pid, uint64_t pid_base, const double *x, const double *y,
+                       const double *vx, const double *vy, uint8_t *rec, void *stream) {
+    clear_error();
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(x && y && vx && vy && rec, "NULL particle array or record buffer");
+    CBRNG_REQUIRE(((uintptr_t)rec & 7) == 0, "record buffer must be 8-byte aligned");
+    auto k = pack_records_kernel;
+    k<<<grid_for(k, 256, 0, (n + 255) / 256), 256, 0, as_stream(stream)>>>(n, pid, pid_base, x, y, vx, vy,
+                                                                           (uint64_t *)rec);
+    return check_launch("pack_records_kernel");
+}
+
+int cbrng_unpack_records(uint64_t n, const uint8_t *rec, uint64_t *pid, double *x, double *y, double *vx,
+                         double *vy, void *stream) {
+    clear_error();
+    if (n == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(x && y && vx && vy && rec, "NULL particle array or record buffer");
+    CBRNG_REQUIRE(((uintptr_t)rec & 7) == 0, "record buffer must be 8-byte aligned");
+    auto k = unpack_records_kernel;
+    k<<<grid_for(k, 256, 0, (n + 255) / 256), 256, 0, as_stream(stream)>>>(n, (const uint64_t *)rec, pid, x, y,
+                                                                           vx, vy);
+    return check_launch("unpack_records_kernel");
+}
+
+int cbrng_pid_order_check(uint64_t n, const uint64_t *pid, uint32_t *bad, void *stream) {
+    clear_error();
+    CBRNG_REQUIRE(bad, "bad is NULL");
+    if (n < 2 || !pid) return CBRNG_OK;
+    auto k = pid_order_kernel;
+    k<<<grid_for(k, 256, 0, (n + 255) / 256), 256, 0, as_stream(stream)>>>(n, pid, bad);
+    return check_launch("pid_order_kernel");
 }
 
 }  // extern "C"

@@ -150,16 +150,17 @@ static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
 }
 
 // Units per thread per tile (independent cipher chains in flight per thread).
-// Default 8 for every algorithm and output (B200 sweep, profiles/r1o_tune.md:
-// Philox 6411 -> 6575 GB/s, Squares 4329 -> 4416, Box-Muller 2526 -> 2655 from
-// 4 to 8). CBRNG_FILL_ILP=1|2|4|8|16 overrides for tuning runs.
+// B200 sweeps: 4 -> 8 lifts Philox 6411 -> 6575 GB/s, Squares 4329 -> 4416,
+// Box-Muller 2526 -> 2655 (profiles/r1o_tune.md); 8 -> 16 adds ~1 % for the
+// Philox / Threefry word and f32 fills and costs Squares 1.5 % (r1p_tune.md).
+// CBRNG_FILL_ILP=1|2|4|8|16 overrides for tuning runs.
 template <int ALG, int OUT>
 static int fill_ilp() {
     static int v = [] {
         const char *e = getenv("CBRNG_FILL_ILP");
         // Box-Muller included: more pairs per thread hide the long FP64
         // dependency chains (ncu r1e at one pair: issue 64 %, "wait" the top stall).
-        const int dflt = 8;
+        const int dflt = ((ALG == PHILOX || ALG == THREEFRY) && (OUT == OUT_U32 || OUT == OUT_F32)) ? 16 : 8;
         int x = e ? atoi(e) : dflt;
         return (x == 1 || x == 2 || x == 4 || x == 8 || x == 16) ? x : dflt;
     }();

@@ -278,6 +278,38 @@ class TestBrownian:
         resumed = cb.run_sim(cb.SimConfig(300, 10), particles=particles, start_iteration=next_it)
         assert resumed.checksum == full.checksum
 
+    @pytest.mark.parametrize("explicit_pid", [False, True])
+    def test_packed_records_match_host_layout(self, cb, oracle, explicit_pid):
+        """cbrng_pack_records == numpy's `<Qdddd` records (brownian.py:209-223), and
+        load_snapshot's device unpack inverts it."""
+        import torch
+        from paper_2310_19925_b200 import brownian
+
+        cfg = cb.SimConfig(1003, 5, algorithm="squares")
+        p = cb.run_sim(cfg, with_checksum=False).particles
+        if explicit_pid:
+            p = brownian.Particles(torch.arange(7, 7 + 3 * p.n, 3, device="cuda").to(torch.uint64),
+                                   p.x, p.y, p.vx, p.vy)
+        h = p.host()
+        want = np.ascontiguousarray(np.column_stack(
+            [h["pid"].astype("<u8")] + [h[k].astype("<f8").view("<u8") for k in ("x", "y", "vx", "vy")]))
+        got = brownian._packed_records(p)
+        assert got.tobytes() == want.tobytes()
+        assert str(brownian.checksum(p)) == f"{oracle.fnv1a64(want.view(np.uint8).ravel()):016x}"
+
+    def test_checksum_rejects_unsorted_pids(self, cb):
+        import torch
+        from paper_2310_19925_b200 import brownian
+
+        p = cb.init_particles(cb.SimConfig(64, 1))
+        pid = torch.arange(64, device="cuda").to(torch.uint64)
+        pid[40], pid[41] = 41, 40
+        with pytest.raises(ValueError):
+            brownian.checksum(brownian.Particles(pid, p.x, p.y, p.vx, p.vy))
+        pid[40], pid[41] = 40, 40
+        with pytest.raises(ValueError):
+            brownian.checksum(brownian.Particles(pid, p.x, p.y, p.vx, p.vy))
+
     def test_shard_invariance_and_stats(self, cb):
         """pid-range shards (any count) reproduce the single run bit for bit."""
         import torch

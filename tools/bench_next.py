@@ -44,4 +44,15 @@ with open("/dev/null", "wb") as sink:
     t0 = time.perf_counter()
     nbytes = emit.emit_words(make_generator("philox", 1, 0), 1 << 30, sink)
     res["emit_raw_GBps"] = round(nbytes / (time.perf_counter() - t0) / 1e9, 2)
+
+# §8(f) rank 3: snapshot records / checksum of 10M particles (cfg3 state)
+from paper_2310_19925_b200 import brownian  # noqa: E402
+
+cfg = brownian.SimConfig(10_000_000, 1)
+p = brownian.init_particles(cfg)
+t = timed(lambda: brownian._packed_records(p), reps=3)
+res["pack_records_10M_to_host_s"] = round(t, 4)
+t0 = time.perf_counter()
+brownian.checksum(p)
+res["checksum_10M_s"] = round(time.perf_counter() - t0, 3)
 print(json.dumps(res))
