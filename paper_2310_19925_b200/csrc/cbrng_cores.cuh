@@ -319,6 +319,21 @@ __device__ __forceinline__ uint32_t addp(uint32_t a, uint32_t b, uint32_t one) {
     }
 }
 
+// Key injection J with the adds forced onto the multiplier (ADDMUL); kj3[j] =
+// ks[(j+3)%5] + j precomputed, so each injection is exactly four IMADs.
+template <int J, bool ADDMUL>
+__device__ __forceinline__ void threefry_inject_m(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3,
+                                                  const uint32_t ks[5], const uint32_t *kj3, uint32_t one) {
+    if constexpr (ADDMUL) {
+        x0 = addp<true>(x0, ks[(J + 0) % 5], one);
+        x1 = addp<true>(x1, ks[(J + 1) % 5], one);
+        x2 = addp<true>(x2, ks[(J + 2) % 5], one);
+        x3 = addp<true>(x3, kj3[J], one);
+    } else {
+        threefry_inject<J>(x0, x1, x2, x3, ks);
+    }
+}
+
 template <int R, int NMUL, bool ADDMUL>
 __device__ __forceinline__ void threefry_round_m(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3,
                                                  const uint32_t *p2, uint32_t one) {
@@ -333,13 +348,15 @@ __device__ __forceinline__ void threefry_round_m(uint32_t &x0, uint32_t &x1, uin
     }
 }
 
-template <int FIRST, int NMUL, bool ADDMUL = false>
+// INJMUL: the key-injection adds forced onto the multiplier as well.
+template <int FIRST, int NMUL, bool ADDMUL = false, bool INJMUL = false>
 __device__ __forceinline__ void threefry_rounds_m(uint32_t &x0, uint32_t &x1, uint32_t &x2, uint32_t &x3,
-                                                  const uint32_t ks[5], const uint32_t *p2, uint32_t one = 1) {
-#define TF_RM(R)                                                                \
-    if (R >= FIRST) {                                                           \
-        threefry_round_m<R, NMUL, ADDMUL>(x0, x1, x2, x3, p2, one);             \
-        if ((R + 1) % 4 == 0) threefry_inject<(R + 1) / 4>(x0, x1, x2, x3, ks); \
+                                                  const uint32_t ks[5], const uint32_t *p2, uint32_t one = 1,
+                                                  const uint32_t *kj3 = nullptr) {
+#define TF_RM(R)                                                                                     \
+    if (R >= FIRST) {                                                                                \
+        threefry_round_m<R, NMUL, ADDMUL>(x0, x1, x2, x3, p2, one);                                  \
+        if ((R + 1) % 4 == 0) threefry_inject_m<(R + 1) / 4, INJMUL>(x0, x1, x2, x3, ks, kj3, one); \
     }
     TF_RM(0) TF_RM(1) TF_RM(2) TF_RM(3) TF_RM(4) TF_RM(5) TF_RM(6) TF_RM(7) TF_RM(8) TF_RM(9)
     TF_RM(10) TF_RM(11) TF_RM(12) TF_RM(13) TF_RM(14) TF_RM(15) TF_RM(16) TF_RM(17) TF_RM(18) TF_RM(19)
@@ -357,6 +374,7 @@ struct ThreefryStream {
     uint32_t x3r;   // rotl(x3_0, 11) (round 1)
     uint32_t p2[16];  // 2^R[r%8] multipliers for rotx<true>
     uint32_t one;     // 1, opaque to the compiler (addp<true>)
+    uint32_t kj3[6];  // ks[(j+3)%5] + j: the x3 term of key injection j
 };
 
 __host__ __device__ inline ThreefryStream threefry_stream_setup(uint64_t seed, uint32_t sc) {
@@ -372,10 +390,11 @@ __host__ __device__ inline ThreefryStream threefry_stream_setup(uint64_t seed, u
     const int ROT[8][2] = {{10, 26}, {11, 21}, {13, 27}, {23, 5}, {6, 20}, {17, 11}, {25, 10}, {18, 20}};
     for (int i = 0; i < 8; i++) { p.p2[2 * i] = 1u << ROT[i][0]; p.p2[2 * i + 1] = 1u << ROT[i][1]; }
     p.one = 1;
+    for (int j = 0; j < 6; j++) p.kj3[j] = p.ks[(j + 3) % 5] + (uint32_t)j;
     return p;
 }
 
-template <int NMUL = 0, bool ADDMUL = false>
+template <int NMUL = 0, bool ADDMUL = false, bool INJMUL = false>
 __device__ __forceinline__ uint4 threefry_stream_block(const ThreefryStream& p, uint32_t bc) {
     // round 0 (even; rot 10, 26): x = (bc+ks0, ks1, ks2, ks3)
     uint32_t x0 = bc + p.s01;
@@ -386,7 +405,7 @@ __device__ __forceinline__ uint4 threefry_stream_block(const ThreefryStream& p, 
     uint32_t x3 = p.x3r ^ x0;
     uint32_t x2 = p.x2_0 + x1;
     x1 = rotl32(x1, 21) ^ x2;
-    threefry_rounds_m<2, NMUL, ADDMUL>(x0, x1, x2, x3, p.ks, p.p2, p.one);
+    threefry_rounds_m<2, NMUL, ADDMUL, INJMUL>(x0, x1, x2, x3, p.ks, p.p2, p.one, p.kj3);
     return make_uint4(x0, x1, x2, x3);
 }
 
@@ -530,6 +549,47 @@ __device__ __forceinline__ float u32_to_f32_alu(uint32_t w) {
 // multiply back into a shift.
 __device__ __forceinline__ float u32_to_f32_mul(uint32_t w, uint32_t m24) {
     return (float)__umulhi(w, m24) * 0x1p-24f;
+}
+
+// int -> float on the XU pipe. For m < 2^24 every rounding mode gives the
+// exact value; ptxas lowers the directed-rounding cvt to the legacy I2F (XU,
+// otherwise idle in these kernels) where cvt.rn becomes I2FP on the ALU pipe.
+__device__ __forceinline__ float u24_to_f32_xu(uint32_t m) {
+    float f;
+    asm("cvt.rm.f32.u32 %0, %1;" : "=f"(f) : "r"(m));
+    return f;
+}
+
+// The exact map (w >> 8) * 2^-24, with its three steps (shift, convert, scale)
+// placed on whichever pipes a kernel has spare (profiles/r1r_tune.md):
+//   CV 0: SHF (alu)       + I2FP (alu) + FMUL (fma)
+//   CV 1: IMAD.HI (heavy) + I2FP (alu) + FMUL (fma)      [u32_to_f32_mul]
+//   CV 2: SHF (alu)       + I2FP (alu) + exponent IADD + max (alu)
+//   CV 3: IMAD.HI (heavy) + I2F (xu)   + FMUL (fma)
+//   CV 4: SHF (alu)       + I2F (xu)   + FMUL (fma)
+//   CV 5: SHF (alu)       + I2F (xu)   + exponent IADD + max (alu)
+template <int CV>
+__device__ __forceinline__ float u32_to_f32_cv(uint32_t w, uint32_t m24) {
+    if constexpr (CV == 0) {
+        return u32_to_f32(w);
+    } else if constexpr (CV == 1) {
+        return u32_to_f32_mul(w, m24);
+    } else if constexpr (CV == 2) {
+        return u32_to_f32_alu(w);
+    } else if constexpr (CV == 3) {
+        return u24_to_f32_xu(__umulhi(w, m24)) * 0x1p-24f;
+    } else if constexpr (CV == 4) {
+        return u24_to_f32_xu(w >> 8) * 0x1p-24f;
+    } else {
+        const int b = __float_as_int(u24_to_f32_xu(w >> 8)) - (24 << 23);
+        return __int_as_float(max(b, 0));
+    }
+}
+
+template <int CV>
+__device__ __forceinline__ float4 u32x4_to_f32x4(uint4 w, uint32_t m24) {
+    return make_float4(u32_to_f32_cv<CV>(w.x, m24), u32_to_f32_cv<CV>(w.y, m24), u32_to_f32_cv<CV>(w.z, m24),
+                       u32_to_f32_cv<CV>(w.w, m24));
 }
 
 // uniform_f64: ((lo | hi<<32) >> 11) * 2^-53, low word first.

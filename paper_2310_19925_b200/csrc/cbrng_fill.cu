@@ -36,24 +36,13 @@ struct FillArgs {
     uint32_t m24;      // 1 << 24 at run time (u32_to_f32_mul)
 };
 
-// MULSHIFT: 0 = shift + FMUL, 1 = shift on the multiplier (ALU-bound kernels),
-// 2 = exponent arithmetic on the ALU (FMA-heavy-bound kernels).
-template <int OUT, int MULSHIFT = 0>
+// CV: where the f32 map's shift / convert / scale run (u32_to_f32_cv).
+template <int OUT, int CV = 0>
 __device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0) {
     if constexpr (OUT == OUT_U32) {
         __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
     } else if constexpr (OUT == OUT_F32) {
-        if constexpr (MULSHIFT == 2) {
-            __stcs(reinterpret_cast<float4 *>(out0) + u,
-                   make_float4(u32_to_f32_alu(w.x), u32_to_f32_alu(w.y), u32_to_f32_alu(w.z), u32_to_f32_alu(w.w)));
-        } else if constexpr (MULSHIFT == 1) {
-            __stcs(reinterpret_cast<float4 *>(out0) + u,
-                   make_float4(u32_to_f32_mul(w.x, m24), u32_to_f32_mul(w.y, m24), u32_to_f32_mul(w.z, m24),
-                               u32_to_f32_mul(w.w, m24)));
-        } else {
-            __stcs(reinterpret_cast<float4 *>(out0) + u,
-                   make_float4(u32_to_f32(w.x), u32_to_f32(w.y), u32_to_f32(w.z), u32_to_f32(w.w)));
-        }
+        __stcs(reinterpret_cast<float4 *>(out0) + u, u32x4_to_f32x4<CV>(w, m24));
     } else if constexpr (OUT == OUT_F64) {
         __stcs(reinterpret_cast<double2 *>(out0) + u, make_double2(u32x2_to_f64(w.x, w.y), u32x2_to_f64(w.z, w.w)));
     } else {
@@ -77,7 +66,7 @@ __device__ __forceinline__ void store_tail(void *out0, uint64_t u, uint32_t tail
     }
 }
 
-template <int ALG, int OUT, int ILP, bool SKIP, int V>
+template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV>
 __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -93,7 +82,7 @@ __global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillA
         for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, base + 32 * j);
 #pragma unroll
         for (int j = 0; j < ILP; j++)
-            store_unit<OUT, ALG == THREEFRY ? 1 : 0>(a.out0, a.out1, base + 32 * j, w[j], a.m24);
+            store_unit<OUT, CV>(a.out0, a.out1, base + 32 * j, w[j], a.m24);
     }
     // Remainder (< one tile) and the partial trailing unit: the last warp of the grid.
     if (warp == nwarps - 1) {
@@ -140,78 +129,108 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
 
 constexpr int FILL_BLOCK = 256;
 
-template <int ALG, int OUT, bool SKIP, int ILP, int V>
+template <int ALG, int OUT, bool SKIP, int ILP, int V, int CV>
 static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
-    auto k = fill_kernel<ALG, OUT, ILP, SKIP, V>;
+    auto k = fill_kernel<ALG, OUT, ILP, SKIP, V, CV>;
     uint64_t work = (a.n_units + (FILL_BLOCK * ILP) - 1) / (FILL_BLOCK * ILP);
     unsigned grid = grid_for(k, FILL_BLOCK, 0, work ? work : 1);
     k<<<grid, FILL_BLOCK, 0, st>>>(a);
     return check_launch("fill_kernel");
 }
 
+static int env_knob(const char *name, int dflt, int lo, int hi) {
+    const char *e = getenv(name);
+    const int x = e ? atoi(e) : dflt;
+    return (x >= lo && x <= hi) ? x : dflt;
+}
+
 // Units per thread per tile (independent cipher chains in flight per thread).
 // B200 sweeps: 4 -> 8 lifts Philox 6411 -> 6575 GB/s, Squares 4329 -> 4416,
-// Box-Muller 2526 -> 2655 (profiles/r1o_tune.md); 8 -> 16 adds ~1 % for the
-// Philox / Threefry word and f32 fills and costs Squares 1.5 % (r1p_tune.md).
-// CBRNG_FILL_ILP=1|2|4|8|16 overrides for tuning runs.
+// Box-Muller 2526 -> 2655 (profiles/r1o_tune.md); 8 -> 16 adds 2 % for the
+// Philox word and f32 fills and costs Squares 1.5 % (r1p_tune.md) and, with the
+// XU conversion, Threefry 2 % (r1r_tune.md).
+// Box-Muller stays at 8: more pairs per thread hide the long FP64 dependency
+// chains (ncu r1e at one pair: issue 64 %, "wait" the top stall), 16 spills.
+// CBRNG_FILL_ILP=8|16 overrides for tuning runs.
 template <int ALG, int OUT>
 static int fill_ilp() {
     static int v = [] {
-        const char *e = getenv("CBRNG_FILL_ILP");
-        // Box-Muller included: more pairs per thread hide the long FP64
-        // dependency chains (ncu r1e at one pair: issue 64 %, "wait" the top stall).
-        const int dflt = ((ALG == PHILOX || ALG == THREEFRY) && (OUT == OUT_U32 || OUT == OUT_F32)) ? 16 : 8;
-        int x = e ? atoi(e) : dflt;
-        return (x == 1 || x == 2 || x == 4 || x == 8 || x == 16) ? x : dflt;
+        const int dflt = (ALG == PHILOX && (OUT == OUT_U32 || OUT == OUT_F32)) ? 16 : 8;
+        const int x = env_knob("CBRNG_FILL_ILP", dflt, 8, 16);
+        return (OUT == OUT_U32 || OUT == OUT_F32) && x == 16 ? 16 : 8;
     }();
     return v;
 }
 
-// Threefry rotation split (see rotx in cbrng_cores.cuh); CBRNG_TF_VARIANT=0|1|2.
+// Default code variants (B200 sweeps, profiles/r1r_tune.md): Threefry V (see
+// block_at) and the f32 conversion placement CV (see u32_to_f32_cv) per
+// generator. CBRNG_TF_VARIANT=0..6 and CBRNG_CVT=0..5 override for tuning runs.
+constexpr int TF_V_DEFAULT = 4;
+template <int ALG> constexpr int cv_default() { return ALG == SQUARES ? 0 : 4; }
+
 static int tf_variant() {
-    static int v = [] {
-        const char *e = getenv("CBRNG_TF_VARIANT");
-        int x = e ? atoi(e) : 2;  // B200 sweep (profiles/r1d_tune.md): forced-IMAD adds
-        return (x >= 0 && x <= 3) ? x : 2;
-    }();
+    static int v = env_knob("CBRNG_TF_VARIANT", TF_V_DEFAULT, 0, 6);
+    return v;
+}
+template <int ALG>
+static int cv_variant() {
+    static int v = env_knob("CBRNG_CVT", cv_default<ALG>(), 0, 5);
     return v;
 }
 
-template <int ALG, int OUT, bool SKIP, int V>
+template <int ALG, int OUT, bool SKIP, int V, int CV>
 static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
     if constexpr (SKIP) {
-        return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);  // resumed mid-block: rare, 2 blocks per unit
+        return launch_fill_ilp<ALG, OUT, SKIP, 2, V, CV>(a, st);  // resumed mid-block: rare, 2 blocks per unit
     } else {
-        switch (fill_ilp<ALG, OUT>()) {
-            case 1: return launch_fill_ilp<ALG, OUT, SKIP, 1, V>(a, st);
-            case 2: return launch_fill_ilp<ALG, OUT, SKIP, 2, V>(a, st);
-            case 4: return launch_fill_ilp<ALG, OUT, SKIP, 4, V>(a, st);
-            case 16:
-                if constexpr (OUT == OUT_U32 || OUT == OUT_F32) return launch_fill_ilp<ALG, OUT, SKIP, 16, V>(a, st);
-                else return launch_fill_ilp<ALG, OUT, SKIP, 8, V>(a, st);  // 16 spills for the FP64 maps
-            default: return launch_fill_ilp<ALG, OUT, SKIP, 8, V>(a, st);
+        if constexpr (OUT == OUT_U32 || OUT == OUT_F32) {
+            if (fill_ilp<ALG, OUT>() == 16) return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV>(a, st);
+        }
+        return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
+    }
+}
+
+// Tuning dispatch: either the code variant V or the conversion CV departs from
+// its default (never both), which keeps the instantiation count linear.
+template <int ALG, int OUT, bool SKIP, int V0>
+static int launch_fill_cv(const FillArgs<ALG> &a, cudaStream_t st) {
+    constexpr int C0 = cv_default<ALG>();
+    if constexpr (OUT == OUT_F32 && !SKIP) {
+        switch (cv_variant<ALG>()) {
+            case 0: return launch_fill_v<ALG, OUT, SKIP, V0, 0>(a, st);
+            case 1: return launch_fill_v<ALG, OUT, SKIP, V0, 1>(a, st);
+            case 2: return launch_fill_v<ALG, OUT, SKIP, V0, 2>(a, st);
+            case 3: return launch_fill_v<ALG, OUT, SKIP, V0, 3>(a, st);
+            case 4: return launch_fill_v<ALG, OUT, SKIP, V0, 4>(a, st);
+            default: return launch_fill_v<ALG, OUT, SKIP, V0, 5>(a, st);
         }
     }
+    return launch_fill_v<ALG, OUT, SKIP, V0, C0>(a, st);
 }
 
 template <int ALG, int OUT, bool SKIP>
 static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
+    constexpr int C0 = cv_default<ALG>();
     if constexpr (ALG == SQUARES) {
         // counters bc0 .. bc0 + 4*(n_units+1) - 1 never wrap: drop the per-unit check
-        if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) return launch_fill_v<ALG, OUT, SKIP, 1>(a, st);
-        return launch_fill_v<ALG, OUT, SKIP, 0>(a, st);
+        if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) return launch_fill_cv<ALG, OUT, SKIP, 1>(a, st);
+        return launch_fill_v<ALG, OUT, SKIP, 0, C0>(a, st);
     }
-    if constexpr (ALG == THREEFRY && (OUT == OUT_U32 || OUT == OUT_F32)) {
-        switch (tf_variant()) {
-            case 0: return launch_fill_v<ALG, OUT, SKIP, 0>(a, st);
-            case 1: return launch_fill_v<ALG, OUT, SKIP, 1>(a, st);
-            case 2: return launch_fill_v<ALG, OUT, SKIP, 2>(a, st);
-            case 3: return launch_fill_v<ALG, OUT, SKIP, 3>(a, st);
-            default: break;
+    if constexpr (ALG == THREEFRY && (OUT == OUT_U32 || OUT == OUT_F32) && !SKIP) {
+        if (tf_variant() != TF_V_DEFAULT) {
+            switch (tf_variant()) {
+                case 0: return launch_fill_v<ALG, OUT, SKIP, 0, C0>(a, st);
+                case 1: return launch_fill_v<ALG, OUT, SKIP, 1, C0>(a, st);
+                case 2: return launch_fill_v<ALG, OUT, SKIP, 2, C0>(a, st);
+                case 3: return launch_fill_v<ALG, OUT, SKIP, 3, C0>(a, st);
+                case 4: return launch_fill_v<ALG, OUT, SKIP, 4, C0>(a, st);
+                case 5: return launch_fill_v<ALG, OUT, SKIP, 5, C0>(a, st);
+                default: return launch_fill_v<ALG, OUT, SKIP, 6, C0>(a, st);
+            }
         }
     }
-    if constexpr (ALG == THREEFRY) return launch_fill_v<ALG, OUT, SKIP, 2>(a, st);
-    return launch_fill_v<ALG, OUT, SKIP, 0>(a, st);
+    if constexpr (ALG == THREEFRY) return launch_fill_cv<ALG, OUT, SKIP, TF_V_DEFAULT>(a, st);
+    return launch_fill_cv<ALG, OUT, SKIP, 0>(a, st);
 }
 
 template <int ALG, int OUT>

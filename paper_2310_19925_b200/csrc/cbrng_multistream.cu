@@ -10,6 +10,8 @@
 //     8 rows x 64 contiguous bytes (staged_prefix_kernel);
 //   * shorter rows: lanes map to contiguous 16-byte chunks of consecutive rows
 //     (prefix_kernel).
+#include <cstdlib>
+
 #include "cbrng_internal.cuh"
 
 namespace cbrng {
@@ -68,18 +70,13 @@ __device__ __forceinline__ uint32_t single_word(const StreamKey<ALG> &k, uint32_
     }
 }
 
-// OUT: 0 = u32 words, 1 = uniform f32.
-template <int OUT, bool MULSHIFT = false>
+// OUT: 0 = u32 words, 1 = uniform f32 (conversion placement CV, u32_to_f32_cv).
+template <int OUT, int CV = 0>
 __device__ __forceinline__ void store4(void *out, uint64_t word_index, uint4 w, uint32_t m24 = 0) {
     if constexpr (OUT == 0) {
         __stcs(reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(out) + word_index), w);
-    } else if constexpr (MULSHIFT) {
-        __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + word_index),
-               make_float4(u32_to_f32_mul(w.x, m24), u32_to_f32_mul(w.y, m24), u32_to_f32_mul(w.z, m24),
-                           u32_to_f32_mul(w.w, m24)));
     } else {
-        __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + word_index),
-               make_float4(u32_to_f32(w.x), u32_to_f32(w.y), u32_to_f32(w.z), u32_to_f32(w.w)));
+        __stcs(reinterpret_cast<float4 *>(reinterpret_cast<float *>(out) + word_index), u32x4_to_f32x4<CV>(w, m24));
     }
 }
 template <int OUT>
@@ -162,17 +159,16 @@ __device__ __forceinline__ uint32_t ty_slot(uint32_t r, uint32_t c) { return r *
 
 // One thread per stream; a warp transposes its 32 streams x 16 words through
 // shared memory so each global store instruction writes 8 rows x 64 B.
-// VEC: rows are 16-byte aligned (nwords % 4 == 0) -> 128-bit stores. MUL: the
-// f32 shift on the multiplier (ALU-bound generators). Compile-time so the
-// copy-out is branch-free.
+// VEC: rows are 16-byte aligned (nwords % 4 == 0) -> 128-bit stores. CV: the
+// f32 conversion placement (u32_to_f32_cv). Compile-time so the copy-out is
+// branch-free.
 // Occupancy: Tyche's row state is 4 registers (32-register cap, 8 CTAs/SM);
 // the counter-based row generators keep the folded stream setup live (~20
 // registers for Philox: 4 CTAs/SM, <= 64 registers, spill-free), the others 5.
 template <int ALG> constexpr int staged_min_blocks() { return ALG == TYCHE ? 8 : (ALG == PHILOX ? 4 : 5); }
 
-template <int ALG, int OUT, bool VEC>
+template <int ALG, int OUT, bool VEC, int CV>
 __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_kernel(const __grid_constant__ PrefixArgs a) {
-    constexpr bool MUL = ALG == TYCHE || ALG == THREEFRY;
     __shared__ uint4 tile[TY_WARPS][32 * TY_CH];  // 16 KB per CTA: 8 CTAs (64 warps) fit an SM
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -202,7 +198,7 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_k
                 if (rrow + 8 * k < rows_left) {
                     const uint4 v = my[rslot + 32 * k];
                     if constexpr (VEC) {
-                        store4<OUT, MUL>(a.out, at + k * rstride, v, a.m24);
+                        store4<OUT, CV>(a.out, at + k * rstride, v, a.m24);
                     } else {  // rows not 16-byte aligned (nwords % 4 != 0)
                         const uint64_t o = at + k * rstride;
                         store1<OUT>(a.out, o, v.x); store1<OUT>(a.out, o + 1, v.y);
@@ -221,16 +217,41 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_k
     }
 }
 
-template <int ALG, int OUT>
-static int launch_staged(const PrefixArgs &a, cudaStream_t st) {
+template <int ALG, int OUT, int CV>
+static int launch_staged_cv(const PrefixArgs &a, cudaStream_t st) {
     if (a.nwords % 4 == 0) {
-        auto k = staged_prefix_kernel<ALG, OUT, true>;
+        auto k = staged_prefix_kernel<ALG, OUT, true, CV>;
         k<<<grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
     } else {
-        auto k = staged_prefix_kernel<ALG, OUT, false>;
+        auto k = staged_prefix_kernel<ALG, OUT, false, CV>;
         k<<<grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
     }
     return check_launch("staged_prefix_kernel");
+}
+
+// f32 conversion placement per generator (B200 sweep, profiles/r1r_tune.md);
+// CBRNG_CVT_MS=0..5 overrides for tuning runs.
+template <int ALG> constexpr int ms_cv_default() { return ALG == SQUARES ? 0 : 4; }
+
+template <int ALG, int OUT>
+static int launch_staged(const PrefixArgs &a, cudaStream_t st) {
+    constexpr int C0 = ms_cv_default<ALG>();
+    if constexpr (OUT == 1) {
+        static const int cv = [] {
+            const char *e = getenv("CBRNG_CVT_MS");
+            const int x = e ? atoi(e) : C0;
+            return (x >= 0 && x <= 5) ? x : C0;
+        }();
+        switch (cv) {
+            case 0: return launch_staged_cv<ALG, OUT, 0>(a, st);
+            case 1: return launch_staged_cv<ALG, OUT, 1>(a, st);
+            case 2: return launch_staged_cv<ALG, OUT, 2>(a, st);
+            case 3: return launch_staged_cv<ALG, OUT, 3>(a, st);
+            case 4: return launch_staged_cv<ALG, OUT, 4>(a, st);
+            default: return launch_staged_cv<ALG, OUT, 5>(a, st);
+        }
+    }
+    return launch_staged_cv<ALG, OUT, C0>(a, st);
 }
 
 template <int ALG, int OUT>

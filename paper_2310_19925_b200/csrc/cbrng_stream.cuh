@@ -12,17 +12,22 @@ template <> struct StreamOf<THREEFRY> { using T = ThreefryStream; };
 template <> struct StreamOf<SQUARES> { using T = SquaresStream; };
 
 
-// V selects a code variant per algorithm. Threefry: V = 0 compiler-scheduled;
-// V = 1: all round adds forced to IMAD + 10 of 40 rotations on the multiplier;
-// V = 2: all round adds forced to IMAD, rotations on the ALU;
-// V = 3: all round adds forced to IMAD + 6 rotations on the multiplier.
+// V selects a code variant per algorithm. Threefry (adds "forced" = emitted as
+// IMAD on the FMA-heavy pipe instead of IADD3 on the ALU pipe; "mul" rotations
+// = IMAD.WIDE by 2^r instead of SHF.L.W):
+//   V = 0 compiler-scheduled;             V = 1: forced round adds + 10 mul rotations;
+//   V = 2: forced round adds;             V = 3: forced round adds + 6 mul rotations;
+//   V = 4: forced round + injection adds; V = 5/6: V4 + 2/4 mul rotations.
 template <int ALG, int V>
 __device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, uint32_t bc) {
     if constexpr (ALG == PHILOX) return philox_stream_block(p, bc);
     else if constexpr (V == 0) return threefry_stream_block<0, false>(p, bc);
     else if constexpr (V == 1) return threefry_stream_block<10, true>(p, bc);
     else if constexpr (V == 2) return threefry_stream_block<0, true>(p, bc);
-    else return threefry_stream_block<6, true>(p, bc);
+    else if constexpr (V == 3) return threefry_stream_block<6, true>(p, bc);
+    else if constexpr (V == 4) return threefry_stream_block<0, true, true>(p, bc);
+    else if constexpr (V == 5) return threefry_stream_block<2, true, true>(p, bc);
+    else return threefry_stream_block<4, true, true>(p, bc);
 }
 
 template <int ALG, bool SKIP, int V = 0>

@@ -1,0 +1,72 @@
+"""Every tuning variant of the fill kernels is bit-exact, not just the default.
+
+The code variants (Threefry round/injection/rotation pipe placement,
+CBRNG_TF_VARIANT; f32 conversion placement, CBRNG_CVT / CBRNG_CVT_MS; ILP,
+CBRNG_FILL_ILP) are selected by environment knobs read once per process, so
+each combination runs in a fresh child process and is compared with the CPU
+oracle (the reference's algorithm, pinned to golden vectors in test_oracle.py).
+Sizes cover full warp tiles, the remainder path and a ragged tail.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+CHILD = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2310_19925_b200 as cb
+from paper_2310_19925_b200 import bulk
+from oracle import oracle as orc
+bad = []
+for alg in ("philox", "threefry", "squares"):
+    for n in (4 * 32 * 16 * 3 + 4 * 37 + 3, 1 << 20):
+        got = cb.uniform_f32_array(cb.make_generator(alg, 0xDEADBEEF1234, 7), n).cpu().numpy()
+        ref = orc.words_to_f32(orc.stream_words(alg, 0xDEADBEEF1234, 7, n))
+        if not np.array_equal(got, ref): bad.append(f"f32 {alg} {n}")
+        w = cb.make_generator(alg, 99, 3).words(n).cpu().numpy()
+        if not np.array_equal(w, orc.stream_words(alg, 99, 3, n)): bad.append(f"u32 {alg} {n}")
+for alg in ("tyche", "threefry", "philox", "squares"):
+    got = bulk.prefix_uniform_f32(alg, range(100, 100 + 777), 5, 52).cpu().numpy().reshape(-1)
+    ref = orc.words_to_f32(orc.prefix_words_arange(alg, 100, 777, 5, 52))
+    if not np.array_equal(got, ref): bad.append(f"prefix f32 {alg}")
+print(json.dumps(bad))
+"""
+
+
+def _run(env_extra):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-c", CHILD % str(ROOT)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("cv", range(6))
+def test_f32_conversion_variants(cv):
+    assert _run({"CBRNG_CVT": str(cv), "CBRNG_CVT_MS": str(cv)}) == []
+
+
+@pytest.mark.parametrize("v", range(7))
+def test_threefry_variants(v):
+    assert _run({"CBRNG_TF_VARIANT": str(v)}) == []
+
+
+@pytest.mark.parametrize("ilp", [8, 16])
+def test_ilp_variants(ilp):
+    assert _run({"CBRNG_FILL_ILP": str(ilp)}) == []

@@ -1,6 +1,7 @@
 """Time the configs[1] fills under code variants (env knobs read once per process).
 
-    python tools/tune_fills.py            # sweeps CBRNG_FILL_ILP x CBRNG_TF_VARIANT
+    python tools/tune_fills.py            # sweeps CBRNG_FILL_ILP x CBRNG_GRID_MULT x CBRNG_TF_VARIANT
+    TUNE_SETS="CBRNG_CVT=1;CBRNG_CVT=3,CBRNG_CVT_MS=3" python tools/tune_fills.py   # explicit env sets
 """
 import itertools
 import json
@@ -46,17 +47,24 @@ print(json.dumps(res))
 '''
 
 rows = []
-GRID = [int(x) for x in os.environ.get("TUNE_GRID", "1,2,0").split(",")]
-ILPS = [int(x) for x in os.environ.get("TUNE_ILP", "2,4").split(",")]
-TFV = [int(x) for x in os.environ.get("TUNE_TF", "2").split(",")]
-for ilp, gm, tfv in itertools.product(ILPS, GRID, TFV):
-    env = dict(os.environ, CBRNG_FILL_ILP=str(ilp), CBRNG_TF_VARIANT=str(tfv), CBRNG_GRID_MULT=str(gm))
+if os.environ.get("TUNE_SETS"):
+    # explicit env sets: "CBRNG_TF_VARIANT=4,CBRNG_CVT=3;CBRNG_CVT=1;..."
+    sets = [dict(kv.split("=") for kv in grp.split(",") if kv) for grp in os.environ["TUNE_SETS"].split(";")]
+else:
+    GRID = [int(x) for x in os.environ.get("TUNE_GRID", "8").split(",")]
+    ILPS = [int(x) for x in os.environ.get("TUNE_ILP", "16").split(",")]
+    TFV = [int(x) for x in os.environ.get("TUNE_TF", "4").split(",")]
+    sets = [{"CBRNG_FILL_ILP": str(i), "CBRNG_GRID_MULT": str(g), "CBRNG_TF_VARIANT": str(t)}
+            for i, g, t in itertools.product(ILPS, GRID, TFV)]
+for knobs in sets:
+    env = dict(os.environ, **knobs)
     r = subprocess.run([sys.executable, "-c", CHILD % str(ROOT)], env=env, capture_output=True, text=True)
     if r.returncode:
         print(r.stderr[-2000:])
         continue
     d = json.loads(r.stdout.strip().splitlines()[-1])
-    rows.append((ilp, gm, tfv, d))
-    print(f"ILP={ilp} GRID_MULT={gm} TF={tfv} " + " ".join(f"{k}={v['gbs']}" for k, v in d.items()), flush=True)
+    rows.append((knobs, d))
+    tag = " ".join(f"{k.replace('CBRNG_', '')}={v}" for k, v in knobs.items()) or "defaults"
+    print(f"{tag}: " + " ".join(f"{k}={v['gbs']}" for k, v in d.items()), flush=True)
 Path(ROOT / "gpurun_out").mkdir(exist_ok=True)
 (ROOT / "gpurun_out" / "tune_fills.json").write_text(json.dumps(rows, indent=1))
