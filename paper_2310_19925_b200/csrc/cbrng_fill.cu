@@ -66,8 +66,9 @@ __device__ __forceinline__ void store_tail(void *out0, uint64_t u, uint32_t tail
     }
 }
 
-template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV>
-__global__ void __launch_bounds__(256) fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
+// MB: minimum resident CTAs per SM for the register allocator (0 = unconstrained).
+template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV, int MB = 0>
+__global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -129,9 +130,9 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
 
 constexpr int FILL_BLOCK = 256;
 
-template <int ALG, int OUT, bool SKIP, int ILP, int V, int CV>
+template <int ALG, int OUT, bool SKIP, int ILP, int V, int CV, int MB = 0>
 static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
-    auto k = fill_kernel<ALG, OUT, ILP, SKIP, V, CV>;
+    auto k = fill_kernel<ALG, OUT, ILP, SKIP, V, CV, MB>;
     uint64_t work = (a.n_units + (FILL_BLOCK * ILP) - 1) / (FILL_BLOCK * ILP);
     unsigned grid = grid_for(k, FILL_BLOCK, 0, work ? work : 1);
     k<<<grid, FILL_BLOCK, 0, st>>>(a);
@@ -166,6 +167,7 @@ static int fill_ilp() {
 // block_at) and the f32 conversion placement CV (see u32_to_f32_cv) per
 // generator. CBRNG_TF_VARIANT=0..6 and CBRNG_CVT=0..5 override for tuning runs.
 constexpr int TF_V_DEFAULT = 4;
+constexpr int BM_MINB_DEFAULT = 0;
 template <int ALG> constexpr int cv_default() { return ALG == SQUARES ? 0 : 4; }
 
 static int tf_variant() {
@@ -185,6 +187,14 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
     } else {
         if constexpr (OUT == OUT_U32 || OUT == OUT_F32) {
             if (fill_ilp<ALG, OUT>() == 16) return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV>(a, st);
+        }
+        if constexpr (OUT == OUT_NORMAL) {
+            // register cap for the FP64 Box-Muller (CBRNG_BM_MINB: CTAs/SM the
+            // allocator must fit; 0 = unconstrained, 52 registers, 4 CTAs/SM)
+            static const int mb = env_knob("CBRNG_BM_MINB", BM_MINB_DEFAULT, 0, 8);
+            if (mb == 5) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, 5>(a, st);
+            if (mb == 6) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, 6>(a, st);
+            if (mb == 8) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, 8>(a, st);
         }
         return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
     }
