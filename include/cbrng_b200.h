@@ -86,6 +86,12 @@ int cbrng_normal2_f64(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word
                       const uint32_t *tyche_state, uint64_t n_pairs, double *z0, double *z1,
                       uint32_t *tyche_state_out, void *stream);
 
+/* Box-Muller of caller-supplied words, 4 per pair (normal2, distributions.py:72-81,
+ * applied to any word source: the reference's scripted-generator tests,
+ * test_distributions.py:29-40, 178-186). words [dev, u32, 16-byte aligned],
+ * z0/z1 [dev, f64]. Same arithmetic and tolerance as cbrng_normal2_f64. */
+int cbrng_normal2_from_words(const uint32_t *words, uint64_t n_pairs, double *z0, double *z1, void *stream);
+
 /* _kernels.tyche_fill (_kernels.py:22-44): state [host, 4 x u64 < 2^32] in/out.
  * SYNCHRONOUS: waits for the stream so the final state is back in `state`. */
 int cbrng_tyche_fill(uint64_t *state, uint64_t n, uint32_t *out, void *stream);

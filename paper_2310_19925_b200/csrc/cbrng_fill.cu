@@ -38,7 +38,8 @@ struct FillArgs {
 
 // CV: where the f32 map's shift / convert / scale run (u32_to_f32_cv).
 template <int OUT, int CV = 0>
-__device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0) {
+__device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0,
+                                           const double4 *bm_tab = nullptr) {
     if constexpr (OUT == OUT_U32) {
         __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
     } else if constexpr (OUT == OUT_F32) {
@@ -47,7 +48,7 @@ __device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, u
         __stcs(reinterpret_cast<double2 *>(out0) + u, make_double2(u32x2_to_f64(w.x, w.y), u32x2_to_f64(w.z, w.w)));
     } else {
         double z0, z1;
-        box_muller_fast(w, z0, z1);
+        box_muller_fast(w, z0, z1, bm_tab);
         __stcs(reinterpret_cast<double *>(out0) + u, z0);
         __stcs(reinterpret_cast<double *>(out1) + u, z1);
     }
@@ -76,6 +77,9 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
     // Full warp tiles: no bounds checks, all ILP cipher evaluations issued
     // before the stores.
     const uint64_t n_full = a.n_units / TILE;
+    // Box-Muller's log table, staged once per CTA (cbrng_bm.cuh)
+    __shared__ double4 s_bm[OUT == OUT_NORMAL ? 128 : 1];
+    if constexpr (OUT == OUT_NORMAL) bm_stage_table(s_bm);
     for (uint64_t t = warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
@@ -83,12 +87,12 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
         for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, base + 32 * j);
 #pragma unroll
         for (int j = 0; j < ILP; j++)
-            store_unit<OUT, CV>(a.out0, a.out1, base + 32 * j, w[j], a.m24);
+            store_unit<OUT, CV>(a.out0, a.out1, base + 32 * j, w[j], a.m24, s_bm);
     }
     // Remainder (< one tile) and the partial trailing unit: the last warp of the grid.
     if (warp == nwarps - 1) {
         for (uint64_t u = n_full * TILE + lane; u < a.n_units; u += 32)
-            store_unit<OUT>(a.out0, a.out1, u, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, u));
+            store_unit<OUT>(a.out0, a.out1, u, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, u), 0, s_bm);
         if (a.tail && lane == 0)
             store_tail<OUT>(a.out0, a.n_units, a.tail, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, a.n_units));
     }
@@ -98,6 +102,8 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
 // one thread walks the chain. Latency-bound (~12 dependent ALU ops per word).
 template <int OUT>
 __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1, uint32_t *state_out) {
+    __shared__ double4 s_bm[OUT == OUT_NORMAL ? 128 : 1];
+    if constexpr (OUT == OUT_NORMAL) bm_stage_table(s_bm);
     uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
     for (uint64_t i = 0; i < n; i++) {
         if constexpr (OUT == OUT_U32) {
@@ -118,13 +124,29 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
             tyche_mix(a, b, c, d); w.z = b;
             tyche_mix(a, b, c, d); w.w = b;
             double z0, z1;
-            box_muller_fast(w, z0, z1);
+            box_muller_fast(w, z0, z1, s_bm);
             reinterpret_cast<double *>(out0)[i] = z0;
             reinterpret_cast<double *>(out1)[i] = z1;
         }
     }
     if (state_out) {
         state_out[0] = a; state_out[1] = b; state_out[2] = c; state_out[3] = d;
+    }
+}
+
+// Box-Muller over caller-supplied words (4 per pair): the transform of
+// normal2 / normal2_array applied to any word source (the reference tests it
+// with scripted generators, test_distributions.py:29-40, 178-186).
+__global__ void __launch_bounds__(256) normal2_words_kernel(const uint4 *__restrict__ w, uint64_t n_pairs,
+                                                            double *__restrict__ z0, double *__restrict__ z1) {
+    __shared__ double4 s_bm[128];
+    bm_stage_table(s_bm);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pairs;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        double a, b;
+        box_muller_fast(w[i], a, b, s_bm);
+        z0[i] = a;
+        z1[i] = b;
     }
 }
 
@@ -167,7 +189,7 @@ static int fill_ilp() {
 // block_at) and the f32 conversion placement CV (see u32_to_f32_cv) per
 // generator. CBRNG_TF_VARIANT=0..6 and CBRNG_CVT=0..5 override for tuning runs.
 constexpr int TF_V_DEFAULT = 4;
-constexpr int BM_MINB_DEFAULT = 0;
+constexpr int BM_MINB_DEFAULT = 8;  // r1s sweep: 0 -> 8 = +4 % (profiles/r1s_tune.md)
 template <int ALG> constexpr int cv_default() { return ALG == SQUARES ? 0 : 4; }
 
 static int tf_variant() {
@@ -188,7 +210,7 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
         if constexpr (OUT == OUT_U32 || OUT == OUT_F32) {
             if (fill_ilp<ALG, OUT>() == 16) return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV>(a, st);
         }
-        if constexpr (OUT == OUT_NORMAL) {
+        if constexpr (OUT == OUT_NORMAL && ALG == PHILOX) {
             // register cap for the FP64 Box-Muller (CBRNG_BM_MINB: CTAs/SM the
             // allocator must fit; 0 = unconstrained, 52 registers, 4 CTAs/SM)
             static const int mb = env_knob("CBRNG_BM_MINB", BM_MINB_DEFAULT, 0, 8);
@@ -327,6 +349,20 @@ int cbrng_normal2_f64(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word
                       uint64_t n_pairs, double *z0, double *z1, uint32_t *tyche_state_out, void *stream) {
     return dispatch_fill<OUT_NORMAL>(alg, seed, stream_ctr, word_pos, tyche_state, n_pairs, z0, z1,
                                      tyche_state_out, stream);
+}
+
+int cbrng_normal2_from_words(const uint32_t *words, uint64_t n_pairs, double *z0, double *z1, void *stream) {
+    clear_error();
+    if (n_pairs == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(words && z0 && z1, "NULL pointer");
+    if (!aligned(words, 16)) {
+        set_error("words pointer not 16-byte aligned");
+        return CBRNG_EALIGN;
+    }
+    cudaStream_t st = as_stream(stream);
+    normal2_words_kernel<<<grid_for(normal2_words_kernel, 256, 0, (n_pairs + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const uint4 *>(words), n_pairs, z0, z1);
+    return check_launch("normal2_words_kernel");
 }
 
 int cbrng_tyche_fill(uint64_t *state, uint64_t n, uint32_t *out, void *stream) {

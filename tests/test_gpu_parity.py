@@ -186,6 +186,34 @@ class TestDistributions:
             ulps = np.abs(got - r) / np.spacing(np.maximum(np.abs(r), 1.0))
             assert ulps.max() <= BM_ULP, ulps.max()
 
+    def test_normal2_words_edges(self, cb, oracle, record_property):
+        """Box-Muller over chosen words: u1 = 1 (r = 0), u1 = 2^-53 (largest r),
+        u1 next to 1 and to binade / log-table boundaries, t on and next to the
+        quadrant boundaries, plus 2^22 random pairs."""
+        rng = np.random.default_rng(2310)
+        u_edges = [0, 1, 2, 3, 0x7FF, 1 << 20, (1 << 52) - 1, 1 << 52, (1 << 52) + 1, (1 << 53) - 1, (1 << 53) - 2,
+                   (1 << 51), 3 << 50, (1 << 53) - (1 << 45), (1 << 53) - (1 << 44) - 1]
+        u2_edges = [0, 1, (1 << 53) - 1] + [(k << 51) + d for k in range(4) for d in (-1, 0, 1) if (k << 51) + d >= 0]
+        pairs = [(u, v) for u in u_edges for v in u2_edges]
+        u_rand = rng.integers(0, 1 << 53, size=(1 << 22), dtype=np.uint64)
+        v_rand = rng.integers(0, 1 << 53, size=(1 << 22), dtype=np.uint64)
+        u_all = np.concatenate([np.array([p[0] for p in pairs], np.uint64), u_rand])
+        v_all = np.concatenate([np.array([p[1] for p in pairs], np.uint64), v_rand])
+        a = u_all << np.uint64(11) | (u_all & np.uint64(0x7FF))  # low 11 bits are dropped by the map
+        b = v_all << np.uint64(11)
+        w = np.empty((u_all.size, 4), np.uint32)
+        w[:, 0], w[:, 1] = (a & np.uint64(0xFFFFFFFF)).astype(np.uint32), (a >> np.uint64(32)).astype(np.uint32)
+        w[:, 2], w[:, 3] = (b & np.uint64(0xFFFFFFFF)).astype(np.uint32), (b >> np.uint64(32)).astype(np.uint32)
+        z0, z1 = (host(z) for z in cb.words_to_normal2(w))
+        r0, r1 = oracle.words_to_normal2(w)
+        worst = 0.0
+        for got, r in ((z0, r0), (z1, r1)):
+            ulps = np.abs(got - r) / np.spacing(np.maximum(np.abs(r), 1.0))
+            worst = max(worst, float(ulps.max()))
+        record_property("box_muller_max_ulp", worst)
+        assert worst <= BM_ULP, worst
+        assert z0[0] == 0 and z1[0] == 0  # u1 == 1 -> r == 0
+
     def test_scalar_forms(self, cb, oracle):
         g = cb.make_generator("threefry", 12, 0)
         w = oracle.stream_words("threefry", 12, 0, 64)
