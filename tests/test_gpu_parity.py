@@ -529,3 +529,16 @@ class TestShardingAndKernelsModule:
         _kernels.philox_block_lanes(seeds, scs, 1, blk)
         assert np.array_equal(blk, oracle.prefix_words("philox", seeds, 4, 8)[:, 4:8])
         assert _kernels.fnv1a64(np.zeros(40, np.uint8)) == oracle.fnv1a64(bytes(40))
+
+
+class TestMicroBenchmark:
+    """The reference's harness-shape tests (pkg/tests/test_bench.py); timings are not asserted."""
+
+    def test_rows(self, cb):
+        rows = cb.micro_benchmark("philox", [1, 10, 100], repetitions=2)
+        assert [r.length for r in rows] == [1, 10, 100]
+        assert all(r.median_ns > 0 and r.words_per_second > 0 and r.algorithm == "philox" for r in rows)
+
+    def test_amortizes(self, cb):
+        rows = cb.micro_benchmark("squares", [1, 1_000_000], repetitions=3)
+        assert rows[1].median_ns / rows[1].length < rows[0].median_ns / rows[0].length

@@ -86,3 +86,25 @@ def test_simconfig_validation():
         with pytest.raises(ValueError):
             SimConfig(**{**dict(n_particles=4, steps=1), **kw})
     assert SimConfig(4, 1, algorithm="tyche").algorithm is G.Algorithm.TYCHE
+
+
+def test_micro_benchmark_validation():
+    """bench.py:36-45 error behaviour (raised before any device work)."""
+    from paper_2310_19925_b200 import micro_benchmark
+
+    with pytest.raises(ValueError):
+        micro_benchmark("philox", [0], repetitions=1)
+    with pytest.raises(ValueError):
+        micro_benchmark("philox", [1], repetitions=0)
+    with pytest.raises(ValueError):
+        micro_benchmark("nonsense", [1])
+
+
+def test_bench_renderers():
+    from paper_2310_19925_b200.microbench import BenchRow, bench_rows_csv, format_bench_table
+
+    rows = [BenchRow("threefry", 1, 1500.0, 6.7e5), BenchRow("threefry", 10, 1600.0, 6.25e6)]
+    table = format_bench_table(rows)
+    assert "threefry" in table and "words/s" in table
+    csv = bench_rows_csv(rows).splitlines()
+    assert csv[0] == "algorithm,length,median_ns,words_per_second" and csv[1].startswith("threefry,1,1500,")

@@ -103,6 +103,18 @@ __global__ void k_i2f64(double *out, uint32_t b) {
     if (s == 12345) out[0] = (double)s;
 }
 
+// IMAD.WIDE alone: 64-bit accumulator chains x = lo32(x) * a + x (mad.wide.u32 with a 64-bit addend).
+__global__ void k_wide(uint64_t *out, uint32_t a) {
+    uint64_t x[CH];
+    for (int c = 0; c < CH; c++) x[c] = threadIdx.x * 7ull + c;
+    for (int i = 0; i < IT; i++)
+#pragma unroll
+        for (int c = 0; c < CH; c++) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(x[c]) : "r"((uint32_t)x[c]), "r"(a));
+    uint64_t s = 0;
+    for (int c = 0; c < CH; c++) s += x[c];
+    if (s == 12345) out[0] = s;
+}
+
 template <typename K, typename... A>
 static void run(const char *name, int per_iter_instr, K k, A... args) {
     int dev = 0, sms = 0, clk = 0;
@@ -140,6 +152,7 @@ int main() {
     run("DFMA + IMAD interleaved (1:1)", 1, k_mix, d, 1.0000001, 1e-9, 0x12345u, 7u);
     run("DFMA + LOP3 interleaved (1:1)", 1, k_mix_alu, d, 1.0000001, 1e-9, 0x12345u, 7u);
     run("I2F.F64.U64 (+IADD 64)", 1, k_i2f64, d, 7u);
+    run("IMAD.WIDE (64-bit addend, alone)", 1, k_wide, (uint64_t *)u, 0x12345u);
     cudaError_t e = cudaDeviceSynchronize();
     printf("# %s\n", cudaGetErrorString(e));
     return 0;
