@@ -164,6 +164,34 @@ __global__ void __launch_bounds__(256, MINB) brownian_steps_kernel(const __grid_
     }
 }
 
+// Fused walk, Philox with pid < 2^32: the two step-uniform multiplies of
+// rounds 0-1 (philox_step_uniform) are computed once per step per CTA into a
+// shared table of TAB steps (one step per thread), so each particle-step runs
+// 16 IMAD.WIDE instead of 18 (the kernel is FMA-heavy-pipe bound). One thread
+// per particle; threads past n take part in the table and the barriers only.
+constexpr int BR_TAB = 256;
+
+template <bool FOLD, int MINB>
+__global__ void __launch_bounds__(256, MINB) brownian_fused_philox_kernel(const __grid_constant__ BrownArgs a) {
+    __shared__ uint4 tab[BR_TAB];
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = i < a.n;
+    const uint64_t pid = live ? (a.pid ? a.pid[i] : a.pid_base + i) : 0;
+    double x = 0.0, y = 0.0, vx = 0.0, vy = 0.0;
+    if (live) { x = a.x[i]; y = a.y[i]; vx = a.vx[i]; vy = a.vy[i]; }
+    const PhiloxParticle<true> P = philox_particle_setup<true>(pid);
+    const uint32_t ctr0 = a.init_ctr + (uint32_t)a.first_it;
+    const uint32_t nsteps = (uint32_t)a.nsteps;
+    for (uint32_t base = 0; base < nsteps; base += BR_TAB) {
+        __syncthreads();  // the previous chunk's table is no longer read
+        for (uint32_t j = threadIdx.x; j < BR_TAB; j += blockDim.x) tab[j] = philox_step_uniform(ctr0 + base + j);
+        __syncthreads();
+        const uint32_t m = nsteps - base < (uint32_t)BR_TAB ? nsteps - base : (uint32_t)BR_TAB;
+        for (uint32_t s = 0; s < m; s++) step_update<FOLD>(x, y, vx, vy, philox_particle_block_u(P, tab[s]), a);
+    }
+    if (live) { a.x[i] = x; a.y[i] = y; a.vx[i] = vx; a.vy[i] = vy; }
+}
+
 // ---------------- deterministic statistics ----------------
 __device__ __forceinline__ int64_t fixq(double v, double scale) { return __double2ll_rn(v * scale); }
 
@@ -222,6 +250,13 @@ __global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint
 template <int ALG, bool HI0, bool FOLD, int MINB>
 static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
     auto k = brownian_steps_kernel<ALG, HI0, FOLD, MINB>;
+    if constexpr (ALG == PHILOX && HI0) {
+        static const bool tab = [] {
+            const char *e = getenv("CBRNG_BROWNIAN_TAB");
+            return e ? atoi(e) != 0 : true;
+        }();
+        if (mode == CBRNG_BROWNIAN_FUSED && tab) k = brownian_fused_philox_kernel<FOLD, MINB>;
+    }
     // One thread per particle: the fused kernel needs every particle resident
     // or queued, so the grid covers n (no persistence).
     const unsigned grid = (unsigned)((a.n + 255) / 256);
@@ -236,10 +271,21 @@ static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
     return check_launch("brownian_steps_kernel");
 }
 
+constexpr int BROWNIAN_MINB_DEFAULT = 5;
+
 template <int ALG, bool HI0, bool FOLD>
 static int launch_steps_k(BrownArgs a, int mode, cudaStream_t st) {
-    if constexpr (!HI0) return launch_steps_kb<ALG, HI0, FOLD, 1>(a, mode, st);  // 64-bit pids: 20 live keys, no cap
-    else return launch_steps_kb<ALG, HI0, FOLD, 5>(a, mode, st);
+    if constexpr (!HI0) {
+        return launch_steps_kb<ALG, HI0, FOLD, 1>(a, mode, st);  // 64-bit pids: 20 live keys, no cap
+    } else {
+        // register cap (CTAs/SM), CBRNG_BROWNIAN_MINB=5|6 overrides for tuning runs
+        static const int mb = [] {
+            const char *e = getenv("CBRNG_BROWNIAN_MINB");
+            return e ? atoi(e) : BROWNIAN_MINB_DEFAULT;
+        }();
+        if (mb == 6) return launch_steps_kb<ALG, HI0, FOLD, 6>(a, mode, st);
+        return launch_steps_kb<ALG, HI0, FOLD, 5>(a, mode, st);
+    }
 }
 
 template <int ALG>

@@ -210,6 +210,37 @@ __device__ __forceinline__ uint4 philox_particle_block(const PhiloxParticle<HI0>
     return make_uint4(c0, c1, c2, c3);
 }
 
+// The same block from rounds 0-1's step-uniform products: with pid < 2^32 (HI0)
+// round 0's c2 = hi(M0*ctr) does not depend on the particle, so both
+// M0*ctr and round 1's M1*c2 are the same for every thread of a step. The
+// fused Brownian kernel computes them once per step per CTA (u = {-, lo(M0*ctr),
+// hi(M1*c2), lo(M1*c2)}) and each particle starts at round 1's xors.
+__device__ __forceinline__ uint4 philox_particle_block_u(const PhiloxParticle<true>& p, uint4 u) {
+    uint32_t c0 = u.z ^ p.k0[1];  // c1 of round 0 == 0
+    uint32_t c1 = u.w;
+    uint32_t c2 = u.y ^ p.q1;     // c3 of round 0 = lo(M0*ctr)
+    uint32_t c3;
+    {
+        uint32_t h0, l0, h1, l1;
+        mulhilo(PHILOX_M0, c0, h0, l0);
+        mulhilo(PHILOX_M1, c2, h1, l1);
+        c0 = h1 ^ c1 ^ p.k0[2];
+        c1 = l1;
+        c2 = h0 ^ p.r2;
+        c3 = l0;
+    }
+#pragma unroll
+    for (int r = 3; r < 10; r++) philox_round(c0, c1, c2, c3, p.k0[r], p.K1(r));
+    return make_uint4(c0, c1, c2, c3);
+}
+
+__host__ __device__ __forceinline__ uint4 philox_step_uniform(uint32_t ctr) {
+    uint32_t mh, ml, h1, l1;
+    mulhilo(PHILOX_M0, ctr, mh, ml);
+    mulhilo(PHILOX_M1, mh, h1, l1);  // c2 = mh ^ K1(0), K1(0) = pid_hi = 0
+    return make_uint4(mh, ml, h1, l1);
+}
+
 // ---------------------------------------------------------------------------
 // Threefry4x32-20 (generators.py:125-154)
 // ---------------------------------------------------------------------------
