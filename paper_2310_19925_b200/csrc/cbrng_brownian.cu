@@ -247,9 +247,11 @@ __global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint
     }
 }
 
+// MINB applies to the fused table kernel; the per-step kernel keeps 5 CTAs/SM
+// (6 spills there).
 template <int ALG, bool HI0, bool FOLD, int MINB>
 static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
-    auto k = brownian_steps_kernel<ALG, HI0, FOLD, MINB>;
+    auto k = brownian_steps_kernel<ALG, HI0, FOLD, (MINB > 5 ? 5 : MINB)>;
     if constexpr (ALG == PHILOX && HI0) {
         static const bool tab = [] {
             const char *e = getenv("CBRNG_BROWNIAN_TAB");
