@@ -108,7 +108,6 @@ __global__ void __launch_bounds__(256) prefix_kernel(const __grid_constant__ Pre
 }
 
 constexpr int TY_WARPS = 8;  // 256 threads
-constexpr int TY_CH = 4;     // staged 16-byte chunks per stream row = 16 words (64 B)
 
 // One stream walked word by word by one thread (the staged kernel below).
 // Counter-based algorithms fold the stream-only rounds once per row
@@ -152,10 +151,6 @@ template <> struct RowGen<TYCHE> {
     }
 };
 
-// Staging slot of (row r, chunk c) in a warp's 32 x 4-chunk tile. The XOR
-// swizzle keeps both the row-wise STS.128 (lane = row) and the column-wise
-// LDS.128 (8 lanes = 2 rows x 4 chunks) conflict-free, without padding.
-__device__ __forceinline__ uint32_t ty_slot(uint32_t r, uint32_t c) { return r * TY_CH + (c ^ ((r >> 1) & 3)); }
 
 // One thread per stream; a warp transposes its 32 streams x 16 words through
 // shared memory so each global store instruction writes 8 rows x 64 B.
@@ -167,36 +162,42 @@ __device__ __forceinline__ uint32_t ty_slot(uint32_t r, uint32_t c) { return r *
 // registers for Philox: 4 CTAs/SM, <= 64 registers, spill-free), the others 5.
 template <int ALG> constexpr int staged_min_blocks() { return ALG == TYCHE ? 8 : (ALG == PHILOX ? 4 : 5); }
 
-template <int ALG, int OUT, bool VEC, int CV>
+// CH: 16-byte chunks staged per row per round: 4 (64 B of each row per store
+// instruction, 8 rows; 16 KB/CTA) or 8 (full 128 B lines, 4 rows; 32 KB/CTA).
+template <int ALG, int OUT, bool VEC, int CV, int CH = 4>
 __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_kernel(const __grid_constant__ PrefixArgs a) {
-    __shared__ uint4 tile[TY_WARPS][32 * TY_CH];  // 16 KB per CTA: 8 CTAs (64 warps) fit an SM
+    static_assert(CH == 4 || CH == 8, "CH");
+    constexpr uint32_t RPI = 32 / CH;  // rows per copy-out instruction
+    __shared__ uint4 tile[TY_WARPS][32 * CH];
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t groups = a.nwords / 16, rem = a.nwords % 16;
+    const uint32_t groups = a.nwords / (4 * CH), rem = a.nwords % (4 * CH);
     uint4 *const my = tile[wib];
-    // Loop-invariant staging slots: lane writes row `lane`, chunk c at wslot(c);
-    // for the copy-out, lane reads row r = 8k + lane/4, chunk lane%4 at rslot + 32k
-    // (the swizzle term (r >> 1) & 3 = (lane >> 3) & 3 does not depend on k).
-    const uint32_t wx = (lane >> 1) & 3;
-    const uint32_t rrow = lane >> 2, rc = lane & 3;
-    const uint32_t rslot = rrow * TY_CH + (rc ^ ((lane >> 3) & 3));
+    // Staging slots (XOR swizzle, conflict-free STS.128 row-wise and LDS.128
+    // column-wise): lane writes row `lane`, chunk c at lane*CH + (c ^ wx); for
+    // the copy-out, lane reads row r = RPI*k + rrow, chunk rc. CH = 4: swizzle
+    // (r >> 1) & 3, independent of k; CH = 8: swizzle r & 7 = rrow ^ 4(k & 1).
+    const uint32_t wx = CH == 4 ? (lane >> 1) & 3 : lane & 7;
+    const uint32_t rrow = lane / CH, rc = lane % CH;
+    const uint32_t rslot = CH == 4 ? rrow * CH + (rc ^ ((lane >> 3) & 3)) : rrow * CH + (rc ^ rrow);
     for (uint64_t s0 = warp * 32; s0 < a.n_streams; s0 += nwarps * 32) {
         const uint64_t sid = s0 + lane;
         const bool valid = sid < a.n_streams;
         RowGen<ALG> gen(valid ? seed_of(a, sid) : 0, valid ? ctr_of(a, sid) : 0);
-        // output word index of (row rrow + 8k, chunk rc) in group g: obase + k*rstride + 16g
+        // output word index of (row rrow + RPI k, chunk rc) in group g: at + k*rstride
         uint64_t at = (s0 + rrow) * a.nwords + rc * 4;
-        const uint64_t rstride = 8ull * a.nwords;
+        const uint64_t rstride = (uint64_t)RPI * a.nwords;
         const uint32_t rows_left = a.n_streams - s0 < 32 ? (uint32_t)(a.n_streams - s0) : 32u;
-        for (uint32_t g = 0; g < groups; g++, at += 16) {
+        for (uint32_t g = 0; g < groups; g++, at += 4 * CH) {
 #pragma unroll
-            for (int c = 0; c < TY_CH; c++) my[lane * TY_CH + (c ^ wx)] = gen.next4();
+            for (int c = 0; c < CH; c++) my[lane * CH + (c ^ wx)] = gen.next4();
             __syncwarp();
 #pragma unroll
-            for (int k = 0; k < 4; k++) {
-                if (rrow + 8 * k < rows_left) {
-                    const uint4 v = my[rslot + 32 * k];
+            for (int k = 0; k < (int)CH; k++) {
+                if (rrow + RPI * k < rows_left) {
+                    const uint32_t slot = CH == 4 ? rslot + 32 * k : (rslot + 32 * k) ^ (4 * (k & 1));
+                    const uint4 v = my[slot];
                     if constexpr (VEC) {
                         store4<OUT, CV>(a.out, at + k * rstride, v, a.m24);
                     } else {  // rows not 16-byte aligned (nwords % 4 != 0)
@@ -212,21 +213,37 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_k
             const uint4 w = gen.next4();  // may run up to 3 words past the row end: discarded
             const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
             if (valid)
-                for (uint32_t q = 0; q < 4 && j + q < rem; q++) store1<OUT>(a.out, sid * a.nwords + groups * 16 + j + q, ws[q]);
+                for (uint32_t q = 0; q < 4 && j + q < rem; q++)
+                    store1<OUT>(a.out, sid * a.nwords + groups * 4 * CH + j + q, ws[q]);
         }
     }
 }
 
-template <int ALG, int OUT, int CV>
-static int launch_staged_cv(const PrefixArgs &a, cudaStream_t st) {
+template <int ALG, int OUT, int CV, int CH>
+static int launch_staged_ch(const PrefixArgs &a, cudaStream_t st) {
     if (a.nwords % 4 == 0) {
-        auto k = staged_prefix_kernel<ALG, OUT, true, CV>;
+        auto k = staged_prefix_kernel<ALG, OUT, true, CV, CH>;
         k<<<grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
     } else {
-        auto k = staged_prefix_kernel<ALG, OUT, false, CV>;
+        auto k = staged_prefix_kernel<ALG, OUT, false, CV, CH>;
         k<<<grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
     }
     return check_launch("staged_prefix_kernel");
+}
+
+// Staging width (CBRNG_TY_CH=4|8 overrides for tuning runs; Tyche only).
+constexpr int TY_CH_DEFAULT = 4;
+
+template <int ALG, int OUT, int CV>
+static int launch_staged_cv(const PrefixArgs &a, cudaStream_t st) {
+    if constexpr (ALG == TYCHE) {
+        static const int ch = [] {
+            const char *e = getenv("CBRNG_TY_CH");
+            return e ? atoi(e) : TY_CH_DEFAULT;
+        }();
+        if (ch == 8) return launch_staged_ch<ALG, OUT, CV, 8>(a, st);
+    }
+    return launch_staged_ch<ALG, OUT, CV, 4>(a, st);
 }
 
 // f32 conversion placement per generator (B200 sweep, profiles/r1r_tune.md);

@@ -70,3 +70,8 @@ def test_threefry_variants(v):
 @pytest.mark.parametrize("ilp", [8, 16])
 def test_ilp_variants(ilp):
     assert _run({"CBRNG_FILL_ILP": str(ilp)}) == []
+
+
+@pytest.mark.parametrize("ch", [4, 8])
+def test_tyche_staging_width(ch):
+    assert _run({"CBRNG_TY_CH": str(ch)}) == []
