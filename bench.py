@@ -353,7 +353,8 @@ def main() -> None:
                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * N_PER_GPU * 4,
                    "api": "uniform_f32_array(make_generator(a, 42, 0), 2^30, out=pinned host) x3 + "
                           "bulk.prefix_uniform_f32(tyche, ..., out=pinned host)",
-                   "note": "host-side wall clock; bound by the PCIe D2H copy of 16 GiB/step"}
+                   "note": "host-side wall clock; 64 MiB chunks with the D2H copy overlapped (bulk.generator_fill -> "
+                           "_dev.pipelined_host_fill); bound by PCIe Gen5 x16 D2H (56 GB/s measured, tools/probes/probe_d2h.py)"}
     del host_out, host_ty
 
     if not (args.quick or args.no_side):

@@ -96,6 +96,54 @@ class Sink:
         return self.dev
 
 
+HOST_CHUNK_BYTES = 64 << 20  # chunk of a pipelined device -> host fill
+
+
+def pinned_host_target(out, n: int, dtype: torch.dtype, device) -> torch.Tensor | None:
+    """The pinned host tensor a fill of n elements can stream into chunk by chunk,
+    or None when the destination is not host memory that can take async copies
+    (device outputs, numpy / pageable buffers, small fills keep the one-shot path)."""
+    if n * torch.empty(0, dtype=dtype).element_size() < 2 * HOST_CHUNK_BYTES:
+        return None
+    if out is None:
+        return torch.empty(n, dtype=dtype, pin_memory=True) if is_host(device) else None
+    if (isinstance(out, torch.Tensor) and not out.is_cuda and out.is_pinned() and out.is_contiguous()
+            and out.dtype == dtype and out.numel() == n):
+        return out.view(-1)
+    return None
+
+
+def pipelined_host_fill(n: int, dtype: torch.dtype, hosts: list, launch, row: int = 1) -> None:
+    """Fill host tensors `hosts` (pinned, n*row elements each) by generating
+    HOST_CHUNK_BYTES chunks into two alternating device buffers per output and
+    copying each to the host on a second stream while the next chunk is
+    generated. Chunked copies also reach ~56 GB/s where one multi-GiB copy
+    gets ~53 (tools/probes/probe_d2h.py). launch(dev_ptrs, first, count,
+    stream_ptr) generates elements [first, first + count) (rows of `row`)."""
+    dev = cuda_device()
+    esz = torch.empty(0, dtype=dtype).element_size()
+    k = max(1, HOST_CHUNK_BYTES // (esz * row))
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    bufs = [[torch.empty(k * row, dtype=dtype, device=dev) for _ in hosts] for _ in range(2)]
+    copied = [None, None]
+    for i, off in enumerate(range(0, n, k)):
+        slot, m = i & 1, min(k, n - off)
+        if copied[slot] is not None:
+            comp.wait_event(copied[slot])  # the slot's previous chunk has left the GPU
+        launch([b.data_ptr() for b in bufs[slot]], off, m, int(comp.cuda_stream))
+        ready = torch.cuda.Event()
+        ready.record(comp)
+        copy.wait_event(ready)
+        with torch.cuda.stream(copy):
+            for h, b in zip(hosts, bufs[slot]):
+                h[off * row:(off + m) * row].copy_(b[:m * row], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(copy)
+        copied[slot] = done
+    copy.synchronize()
+
+
 def to_numpy(x) -> np.ndarray:
     if isinstance(x, torch.Tensor):
         return x.detach().cpu().numpy()

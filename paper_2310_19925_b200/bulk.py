@@ -189,6 +189,20 @@ def prefix_uniform_f32(algorithm, seeds, stream_counters, nvalues: int, *, out=N
     """uniform_f32 map of prefix_words, fused (one word per value)."""
     alg = as_algorithm(algorithm)
     s_t, s_base, c_t, c_scalar, n = _prefix_args(seeds, stream_counters, None if _dev.is_host(device) else device)
+    host = _dev.pinned_host_target(None if out is None else out.reshape(-1) if isinstance(out, torch.Tensor) else out,
+                                   n * nvalues, torch.float32, device) if nvalues else None
+    if host is not None:
+        # host destination, large fill: stream ranges generated in chunks, D2H overlapped
+        fn = _lib.lib().cbrng_prefix_uniform_f32
+
+        def launch(ptrs, first, count, st):
+            sp = None if s_t is None else s_t.data_ptr() + 8 * first
+            cp = None if c_t is None else c_t.data_ptr() + 4 * first
+            _lib.check(fn(int(alg), sp, s_base + first, cp, c_scalar, count, nvalues, ptrs[0], st),
+                       "prefix_uniform_f32")
+
+        _dev.pipelined_host_fill(n, torch.float32, [host], launch, row=nvalues)
+        return out if out is not None else host.numpy().reshape(n, nvalues)
     sink = _dev.Sink(n * nvalues, torch.float32, None if out is None else out.reshape(-1), device)
     if n and nvalues:
         _lib.check(_lib.lib().cbrng_prefix_uniform_f32(int(alg), _dev.ptr(s_t), s_base, _dev.ptr(c_t), c_scalar, n,
@@ -234,6 +248,22 @@ def generator_fill(g: Generator, n_elems: int, kind: str, outs=(None, None), dev
     if n_elems < 0:
         raise ValueError("word count must be non-negative")
     fn_name, wpe, dtype, n_out = _FILL_FN[kind]
+    if g.algorithm is not Algorithm.TYCHE:
+        hosts = [_dev.pinned_host_target(outs[i] if i < len(outs) else None, n_elems, dtype, device)
+                 for i in range(n_out)]
+        if all(h is not None for h in hosts):
+            # host destination, large fill: generate in chunks and overlap the D2H copies
+            fn = getattr(_lib.lib(), fn_name)
+            base = g._word_pos()
+
+            def launch(ptrs, first, count, st):
+                _lib.check(fn(int(g.algorithm), g.seed, g.stream_counter, base + first * wpe, None, count, *ptrs,
+                              None, st), fn_name)
+
+            _dev.pipelined_host_fill(n_elems, dtype, hosts, launch)
+            g._advance(n_elems * wpe)
+            res = [outs[i] if (i < len(outs) and outs[i] is not None) else hosts[i].numpy() for i in range(n_out)]
+            return res[0] if n_out == 1 else tuple(res)
     sinks = [_dev.Sink(n_elems, dtype, outs[i] if i < len(outs) else None, device) for i in range(n_out)]
     if n_elems:
         fn = getattr(_lib.lib(), fn_name)

@@ -214,6 +214,28 @@ class TestDistributions:
         assert worst <= BM_ULP, worst
         assert z0[0] == 0 and z1[0] == 0  # u1 == 1 -> r == 0
 
+    @pytest.mark.parametrize("alg", ["philox", "threefry", "squares"])
+    def test_normal2_long_stream_boundary(self, cb, oracle, alg):
+        """configs[3] long-stream layout across a stream boundary: pair i comes
+        from stream (seed, ctr0 + i div P) at pair i mod P (P = 2^32 pairs,
+        2^30 for Squares), computed from an offset without the pairs before it."""
+        import torch
+
+        from paper_2310_19925_b200 import sharding
+
+        per = sharding.pairs_per_stream(alg)
+        lo, hi, seed, ctr0 = per - 5, per + 7, 42, 0xFFFFFFFF  # the stream counter wraps too
+        z0 = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+        z1 = torch.empty_like(z0)
+        sharding.normal2_long(alg, seed, ctr0, lo, hi, z0, z1)
+        words = []
+        for s, off, k in sharding.stream_segments(lo, hi, per):
+            bc = 4 * off if alg == "squares" else off
+            words.append(oracle.stream_words(alg, seed, (ctr0 + s) & M32, 4 * k, block_ctr=bc))
+        r0, r1 = oracle.words_to_normal2(np.concatenate(words))
+        for got, r in ((host(z0), r0), (host(z1), r1)):
+            assert np.all(np.abs(got - r) <= BM_ULP * np.spacing(np.maximum(np.abs(r), 1.0)))
+
     def test_scalar_forms(self, cb, oracle):
         g = cb.make_generator("threefry", 12, 0)
         w = oracle.stream_words("threefry", 12, 0, 64)
@@ -555,3 +577,48 @@ class TestMicroBenchmark:
     def test_amortizes(self, cb):
         rows = cb.micro_benchmark("squares", [1, 1_000_000], repetitions=3)
         assert rows[1].median_ns / rows[1].length < rows[0].median_ns / rows[0].length
+
+
+class TestHostPipelinedFills:
+    """Large fills into host memory stream chunk by chunk (pipelined D2H); the
+    values and the generator state must equal the one-shot device fill."""
+
+    @pytest.mark.parametrize("alg", ["philox", "threefry", "squares"])
+    def test_uniform_f32_to_pinned_host(self, cb, alg):
+        import torch
+
+        n = (1 << 25) + 12345
+        g_host, g_dev = cb.make_generator(alg, 77, 5), cb.make_generator(alg, 77, 5)
+        for g in (g_host, g_dev):
+            g.next_u32(); g.next_u32(); g.next_u32()  # start mid-block
+        out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        got = cb.uniform_f32_array(g_host, n, out=out)
+        assert got is out
+        ref = host(cb.uniform_f32_array(g_dev, n))
+        assert np.array_equal(out.numpy(), ref)
+        assert g_host.state_bytes() == g_dev.state_bytes()
+        assert g_host.next_u32() == g_dev.next_u32()
+
+    def test_normal2_and_words_to_cpu(self, cb):
+        n = (1 << 24) + 7
+        a = cb.normal2_array(cb.make_generator("philox", 3, 1), n, device="cpu")
+        b = cb.normal2_array(cb.make_generator("philox", 3, 1), n)
+        assert all(isinstance(x, np.ndarray) for x in a)
+        assert np.array_equal(a[0], host(b[0])) and np.array_equal(a[1], host(b[1]))
+        w = cb.make_generator("squares", 9, 2).words((1 << 26) + 1, device="cpu")
+        assert np.array_equal(w, host(cb.make_generator("squares", 9, 2).words((1 << 26) + 1)))
+
+    def test_prefix_uniform_f32_to_pinned_host(self, cb):
+        import torch
+
+        from paper_2310_19925_b200 import bulk
+
+        n, nw = (1 << 17) + 3, 256
+        out = torch.empty(n * nw, dtype=torch.float32, pin_memory=True)
+        bulk.prefix_uniform_f32("tyche", range(11, 11 + n), 4, nw, out=out)
+        ref = host(bulk.prefix_uniform_f32("tyche", range(11, 11 + n), 4, nw)).reshape(-1)
+        assert np.array_equal(out.numpy(), ref)
+        seeds = np.arange(5, 5 + n, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+        got = bulk.prefix_uniform_f32("philox", seeds, 0, nw, device="cpu")
+        assert isinstance(got, np.ndarray) and got.shape == (n, nw)
+        assert np.array_equal(got, host(bulk.prefix_uniform_f32("philox", seeds, 0, nw)))
