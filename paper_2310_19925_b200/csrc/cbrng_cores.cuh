@@ -551,6 +551,23 @@ __host__ __device__ __forceinline__ void tyche_mix(uint32_t& a, uint32_t& b, uin
     c += d; b = rotl32(b ^ c, 7);
 }
 
+// The same mix for a single serial chain (latency-bound): the adds carry an
+// opaque zero third operand, so ptxas emits 3-input IADD3 on the ALU pipe
+// instead of IMAD.IADD on the FMA pipe, and the 12-op dependency chain never
+// pays the cross-pipe latency (+1 cycle per pipe switch, 8 per mix).
+__device__ __forceinline__ uint32_t add3z(uint32_t a, uint32_t b, uint32_t z) {
+    uint32_t r;
+    asm("add.u32 %0, %1, %2;\n\tadd.u32 %0, %0, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(z));
+    return r;
+}
+
+__device__ __forceinline__ void tyche_mix_alu(uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d, uint32_t z) {
+    a = add3z(a, b, z); d = rotl32(d ^ a, 16);
+    c = add3z(c, d, z); b = rotl32(b ^ c, 12);
+    a = add3z(a, b, z); d = rotl32(d ^ a, 8);
+    c = add3z(c, d, z); b = rotl32(b ^ c, 7);
+}
+
 __host__ __device__ __forceinline__ uint4 tyche_init(uint64_t seed, uint32_t sc) {
     uint32_t a = (uint32_t)(seed >> 32), b = (uint32_t)seed, c = TYCHE_INIT_CONST, d = sc;
 #pragma unroll 4

@@ -101,28 +101,28 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
 // Tyche is sequential within a stream (generators.py:221-224; _kernels.py:3-5):
 // one thread walks the chain. Latency-bound (~12 dependent ALU ops per word).
 template <int OUT>
-__global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1, uint32_t *state_out) {
+__global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1, uint32_t *state_out, uint32_t z) {
     __shared__ double4 s_bm[OUT == OUT_NORMAL ? 128 : 1];
     if constexpr (OUT == OUT_NORMAL) bm_stage_table(s_bm);
     uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
     for (uint64_t i = 0; i < n; i++) {
         if constexpr (OUT == OUT_U32) {
-            tyche_mix(a, b, c, d);
+            tyche_mix_alu(a, b, c, d, z);
             reinterpret_cast<uint32_t *>(out0)[i] = b;
         } else if constexpr (OUT == OUT_F32) {
-            tyche_mix(a, b, c, d);
+            tyche_mix_alu(a, b, c, d, z);
             reinterpret_cast<float *>(out0)[i] = u32_to_f32(b);
         } else if constexpr (OUT == OUT_F64) {
-            tyche_mix(a, b, c, d);
+            tyche_mix_alu(a, b, c, d, z);
             uint32_t lo = b;
-            tyche_mix(a, b, c, d);
+            tyche_mix_alu(a, b, c, d, z);
             reinterpret_cast<double *>(out0)[i] = u32x2_to_f64(lo, b);
         } else {
             uint4 w;
-            tyche_mix(a, b, c, d); w.x = b;
-            tyche_mix(a, b, c, d); w.y = b;
-            tyche_mix(a, b, c, d); w.z = b;
-            tyche_mix(a, b, c, d); w.w = b;
+            tyche_mix_alu(a, b, c, d, z); w.x = b;
+            tyche_mix_alu(a, b, c, d, z); w.y = b;
+            tyche_mix_alu(a, b, c, d, z); w.z = b;
+            tyche_mix_alu(a, b, c, d, z); w.w = b;
             double z0, z1;
             box_muller_fast(w, z0, z1, s_bm);
             reinterpret_cast<double *>(out0)[i] = z0;
@@ -299,7 +299,7 @@ static int dispatch_fill(int alg, uint64_t seed, uint32_t sc, uint64_t word_pos,
         CBRNG_REQUIRE(tyche_state != nullptr, "tyche fills need the serial state (tyche_state)");
         uint4 s = make_uint4(tyche_state[0], tyche_state[1], tyche_state[2], tyche_state[3]);
         if (n_elems == 0 && tyche_state_out == nullptr) return CBRNG_OK;
-        tyche_stream_kernel<OUT><<<1, 1, 0, st>>>(s, n_elems, out0, out1, tyche_state_out);
+        tyche_stream_kernel<OUT><<<1, 1, 0, st>>>(s, n_elems, out0, out1, tyche_state_out, 0u);
         return check_launch("tyche_stream_kernel");
     }
     if (alg == SQUARES) seed &= 0xFFFFFFFFull;  // generators.py:256-257

@@ -37,6 +37,13 @@ z0 = torch.empty(1 << 27, dtype=torch.float64, device="cuda"); z1 = torch.empty_
 run("normal2_pairs", lambda: _lib.check(L.cbrng_normal2_f64(0, 42, 0, 0, None, 1 << 27, z0.data_ptr(), z1.data_ptr(), None, s)))
 res["normal2_pairs"]["gbs"] = round(res["normal2_pairs"]["gbs"] / 2, 1)  # run() assumes 4 GiB; 2^27 pairs = 2 GiB
 del z0, z1
+import paper_2310_19925_b200 as cb
+g = cb.make_generator("tyche", 42, 0)
+g.words(1 << 16); torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); w = g.words(1 << 22); e1.record(); e1.synchronize()
+res["tyche_serial_mwords"] = {"gbs": round((1 << 22) / (e0.elapsed_time(e1) / 1e3) / 1e6, 1)}
+del w
 from paper_2310_19925_b200 import brownian
 cfg = brownian.SimConfig(10_000_000, 200)
 p = brownian.init_particles(cfg)
