@@ -32,7 +32,7 @@ if "normal" in which:
 if "brownian" in which:
     cfg = brownian.SimConfig(10_000_000, 100)
     p = brownian.init_particles(cfg)
-    brownian.run_steps(p, cfg)
+    brownian.run_steps(p, cfg)  # fused (brownian_fused_philox_kernel)
     brownian.run_steps(p, brownian.SimConfig(10_000_000, 2, mode="per_step"), start_iteration=101)
 torch.cuda.synchronize()
 print("done")
