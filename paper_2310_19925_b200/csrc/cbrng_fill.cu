@@ -187,13 +187,13 @@ static int fill_ilp() {
 
 // Default code variants (B200 sweeps, profiles/r1r_tune.md): Threefry V (see
 // block_at) and the f32 conversion placement CV (see u32_to_f32_cv) per
-// generator. CBRNG_TF_VARIANT=0..6 and CBRNG_CVT=0..5 override for tuning runs.
+// generator. CBRNG_TF_VARIANT=0..8 and CBRNG_CVT=0..5 override for tuning runs.
 constexpr int TF_V_DEFAULT = 4;
 constexpr int BM_MINB_DEFAULT = 8;  // r1s sweep: 0 -> 8 = +4 % (profiles/r1s_tune.md)
 template <int ALG> constexpr int cv_default() { return ALG == SQUARES ? 0 : 4; }
 
 static int tf_variant() {
-    static int v = env_knob("CBRNG_TF_VARIANT", TF_V_DEFAULT, 0, 6);
+    static int v = env_knob("CBRNG_TF_VARIANT", TF_V_DEFAULT, 0, 8);
     return v;
 }
 template <int ALG>
@@ -257,7 +257,9 @@ static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
                 case 3: return launch_fill_v<ALG, OUT, SKIP, 3, C0>(a, st);
                 case 4: return launch_fill_v<ALG, OUT, SKIP, 4, C0>(a, st);
                 case 5: return launch_fill_v<ALG, OUT, SKIP, 5, C0>(a, st);
-                default: return launch_fill_v<ALG, OUT, SKIP, 6, C0>(a, st);
+                case 6: return launch_fill_v<ALG, OUT, SKIP, 6, C0>(a, st);
+                case 7: return launch_fill_v<ALG, OUT, SKIP, 7, C0>(a, st);
+                default: return launch_fill_v<ALG, OUT, SKIP, 8, C0>(a, st);
             }
         }
     }

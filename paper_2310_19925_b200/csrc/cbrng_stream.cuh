@@ -17,7 +17,7 @@ template <> struct StreamOf<SQUARES> { using T = SquaresStream; };
 // = IMAD.WIDE by 2^r instead of SHF.L.W):
 //   V = 0 compiler-scheduled;             V = 1: forced round adds + 10 mul rotations;
 //   V = 2: forced round adds;             V = 3: forced round adds + 6 mul rotations;
-//   V = 4: forced round + injection adds; V = 5/6: V4 + 2/4 mul rotations.
+//   V = 4: forced round + injection adds; V = 5/6/7/8: V4 + 2/4/6/8 mul rotations.
 template <int ALG, int V>
 __device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, uint32_t bc) {
     if constexpr (ALG == PHILOX) return philox_stream_block(p, bc);
@@ -27,7 +27,9 @@ __device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, ui
     else if constexpr (V == 3) return threefry_stream_block<6, true>(p, bc);
     else if constexpr (V == 4) return threefry_stream_block<0, true, true>(p, bc);
     else if constexpr (V == 5) return threefry_stream_block<2, true, true>(p, bc);
-    else return threefry_stream_block<4, true, true>(p, bc);
+    else if constexpr (V == 6) return threefry_stream_block<4, true, true>(p, bc);
+    else if constexpr (V == 7) return threefry_stream_block<6, true, true>(p, bc);
+    else return threefry_stream_block<8, true, true>(p, bc);
 }
 
 template <int ALG, bool SKIP, int V = 0>

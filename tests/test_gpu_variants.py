@@ -62,7 +62,7 @@ def test_f32_conversion_variants(cv):
     assert _run({"CBRNG_CVT": str(cv), "CBRNG_CVT_MS": str(cv)}) == []
 
 
-@pytest.mark.parametrize("v", range(7))
+@pytest.mark.parametrize("v", range(9))
 def test_threefry_variants(v):
     assert _run({"CBRNG_TF_VARIANT": str(v)}) == []
 
