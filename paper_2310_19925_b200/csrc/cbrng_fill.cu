@@ -83,8 +83,21 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
     for (uint64_t t = warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
+        if constexpr (ALG == SQUARES && V == 1) {
+            // no counter wrap anywhere in the fill: unit u's first product
+            // x = ctr * key steps by 32 units = 128 counters per j with one
+            // 64-bit add (ALU) instead of a 64-bit multiply (FMA-heavy)
+            uint64_t x = (uint64_t)(a.bc0 + 4u * (uint32_t)base) * a.p.key + a.p.base;
+            const uint64_t step = a.p.key << 7;
 #pragma unroll
-        for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, base + 32 * j);
+            for (int j = 0; j < ILP; j++) {
+                w[j] = squares_x4(x, a.p.key);
+                x = add64_opaque(x, step);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < ILP; j++) w[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, base + 32 * j);
+        }
 #pragma unroll
         for (int j = 0; j < ILP; j++)
             store_unit<OUT, CV>(a.out0, a.out1, base + 32 * j, w[j], a.m24, s_bm);
