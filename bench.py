@@ -333,7 +333,8 @@ def main() -> None:
     torch.cuda.empty_cache()
     e2e_steps = 2
     host_out = torch.empty(N_PER_GPU, dtype=torch.float32, pin_memory=True)
-    host_ty = torch.empty(TYCHE_STREAMS * TYCHE_WORDS, dtype=torch.float32, pin_memory=True)
+    assert TYCHE_STREAMS * TYCHE_WORDS == N_PER_GPU
+    host_ty = host_out  # one 4 GiB pinned buffer per rank (8 ranks: 32 GiB of pinned host memory, not 64)
 
     def e2e_step():
         for a in ALGS[:3]:
