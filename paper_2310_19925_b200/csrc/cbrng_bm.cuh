@@ -9,28 +9,28 @@
 // FP64 instructions per pair at the accuracy the parity tests demand
 // (<= 4 ulp(max(|z|,1)) of glibc; 3 is the worst seen over 4e7 random pairs
 // in the host prototype of exactly these formulas, fewer 3-ulp cases than
-// the r1 libm-style version). About 43 FP64 instructions per pair, from 63:
+// the r1 libm-style version). About 39 FP64 instructions per pair, from 63:
 //   u1:   never formed. f64(w0,w1) = u 2^-53 with u = (w >> 11), so
 //         u1 = v 2^-53, v = 2^53 - u an integer in [1, 2^53]: one 64-bit
 //         integer subtract and one I2F (XU pipe); the 2^-53 goes into the
 //         exponent k of the log.
 //   -2 ln u1: table-driven (cbrng_logtab.h, tools/gen_logtab.py): v = 2^k z,
-//         z in [0.6875, 1.375), 128 subintervals with (-2 invc, -2 logc as
-//         hi + lo); s = -2 r = fma(z, -2 invc, 2) exact-ish, |s| <= 2^-7,
-//         -2 ln(1+r) = s + s^2 (1/4 + s/12 + s^2/32 + s^3/80 + s^4/192 + s^5/448)
-//         (the series 2 sum (s/2)^n / n, truncation < 2^-59 relative); the
+//         z in [0.6875, 1.375), 256 subintervals with (-2 invc, -2 logc as
+//         hi + lo); s = -2 r = fma(z, -2 invc, 2) exact-ish, |s| <= 2^-8,
+//         -2 ln(1+r) = s + s^2 (1/4 + s/12 + s^2/32 + s^3/80 + s^4/192)
+//         (the series 2 sum (s/2)^n / n, truncation < 2^-56 relative); the
 //         sum k(-2 ln2_hi) + hi is exact, lo and k(-2 ln2_lo) are added to the
-//         small part: 12 FP64 ops instead of ~25 for the fdlibm form with a
+//         small part: 11 FP64 ops instead of ~25 for the fdlibm form with a
 //         Newton reciprocal. The subinterval just below 1 uses invc = 1, so
 //         r = z - 1 is exact and ln u1 keeps full relative accuracy as u1 -> 1.
-//   sqrt: MUFU.RSQ64H seed, one coupled Newton step for (sqrt, 1/(2 sqrt)),
-//         one residual correction: 8 ops.
+//   sqrt: MUFU.RSQ64H seed, one Newton step for sqrt, one residual
+//         correction with the seed's 1/(2 sqrt): 7 ops.
 //   t:    (2 pi 2^-53) * f64(u2 bits): the same rounded value as (2 pi) * u2
 //         (scaling by 2^-53 is exact on both sides), one DMUL.
-//   sincos: 2-term Cody-Waite reduction by pi/2 (t < 2 pi) with DFMA, fdlibm
-//         k_sin / k_cos minimax kernels on |x| <= pi/4; cos as
-//         fma(x^4, C(x^2), 1 - x^2/2) without fdlibm's extra compensation
-//         (the tolerance allows it): 20 ops.
+//   sincos: quadrant from the integer u2, 2-term Cody-Waite reduction by
+//         pi/2 with DFMA, fdlibm k_sin / k_cos minimax kernels on |x| <= pi/4;
+//         cos as fma(x^4, C(x^2), 1 - x^2/2) without fdlibm's extra
+//         compensation (the tolerance allows it): 18 ops.
 #pragma once
 #include <cstdint>
 
@@ -41,7 +41,7 @@ namespace cbrng {
 struct BmConst {
     double s[6];
     double c[6];
-    double two_over_pi, pio2_hi, pio2_lo;
+    double pio2_hi, pio2_lo;
     double m2ln2_hi, m2ln2_lo;  // -2 ln2 split: ln2_hi a multiple of 2^-43
     double two_pi_2m53;         // (2 pi) * 2^-53, exact scaling of the rounded 2*math.pi
 };
@@ -51,20 +51,21 @@ __constant__ BmConst c_bm = {
      2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10},
     {4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
      -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11},
-    6.36619772367581382433e-01, 1.57079632679489655800e+00, 6.12323399573676603587e-17,
+    1.57079632679489655800e+00, 6.12323399573676603587e-17,
     -2.0 * 0x1.62e42fefa3800p-1, -2.0 * 0x1.ef35793c7673p-45,
     6.283185307179586 * 0x1p-53,
 };
 
 // {-2 invc, -2 logc hi, -2 logc lo, 0} per subinterval (tools/gen_logtab.py).
-__constant__ double4 c_logtab[128] = CBRNG_LOGTAB_INIT;
+constexpr int BM_LOGTAB_N = 256;
+__constant__ double4 c_logtab[BM_LOGTAB_N] = CBRNG_LOGTAB_INIT;
 
 // Fill kernels read the table from shared memory (divergent indices would
 // serialise constant-bank reads); a CTA stages it once.
 __device__ __forceinline__ void bm_stage_table(double4 *s_tab) {
     const double2 *src = reinterpret_cast<const double2 *>(c_logtab);
     double2 *dst = reinterpret_cast<double2 *>(s_tab);
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) dst[i] = src[i];
+    for (uint32_t i = threadIdx.x; i < 2 * BM_LOGTAB_N; i += blockDim.x) dst[i] = src[i];
     __syncthreads();
 }
 
@@ -86,14 +87,13 @@ __device__ __forceinline__ double bm_m2log(uint64_t v, const double4 *tab) {
     const uint32_t hi = (uint32_t)__double2hiint(dv);
     const uint32_t th = hi - 0x3fe60000u;            // bits(dv) - bits(0.6875); the low word of OFF is 0
     const int k = ((int)th >> 20) - 53;              // dv = 2^(k+53) z
-    const uint32_t i = (th >> 13) & 127u;            // top 7 mantissa bits of bits(dv) - OFF
+    const uint32_t i = (th >> 12) & 255u;            // top 8 mantissa bits of bits(dv) - OFF
     const double z = __hiloint2double((int)(hi - (th & 0xfff00000u)), __double2loint(dv));
     const double4 e = tab[i];
     const double kd = (double)k;
     const double s = fma(z, e.x, 2.0);                 // -2 r
     const double w = fma(kd, c_bm.m2ln2_hi, e.y);      // exact
-    double p = fma(s, 1.0 / 448, 1.0 / 192);
-    p = fma(s, p, 1.0 / 80);
+    double p = fma(s, 1.0 / 192, 1.0 / 80);
     p = fma(s, p, 1.0 / 32);
     p = fma(s, p, 1.0 / 12);
     p = fma(s, p, 1.0 / 4);
@@ -110,18 +110,18 @@ __device__ __forceinline__ double bm_sqrt(double a) {
     const double h0 = 0.5 * y0, t = a * y0, g = a * h0;
     const double e = fma(-t, y0, 1.0);  // 1 - a y0^2
     const double r1 = fma(g, e, t);     // sqrt(a), ~2x the seed's bits
-    const double h1 = fma(h0, e, h0);   // 1 / (2 sqrt(a))
-    return fma(h1, fma(-r1, r1, a), r1);
+    // residual correction; the seed's 1/(2 sqrt a) suffices: its error only
+    // scales the ~2^-46 residual
+    return fma(h0, fma(-r1, r1, a), r1);
 }
 
-// sin(t), cos(t) for t in [0, 2*pi).
-__device__ __forceinline__ void sincos_2pi(double t, double &sn, double &cs) {
-    // quadrant q = nearest integer to t*2/pi via the 1.5*2^52 shifter: the
-    // integer lands in the low mantissa bits (no FRND/F2I round trip)
-    const double shifter = 0x1.8p52;
-    const double qs = fma(t, c_bm.two_over_pi, shifter);
-    const int qlo = __double2loint(qs);
-    const double q = qs - shifter;
+// sin(t), cos(t) for t = (2 pi) u2 in [0, 2 pi), u2 = v 2^-53. The quadrant
+// q = round(4 u2) comes from the integer v (XU conversion, no FP64 ops); x =
+// t - q pi/2 is then within pi/4 of 0 up to t's rounding, where the fdlibm
+// kernels are accurate.
+__device__ __forceinline__ void sincos_2pi(double t, uint64_t v, double &sn, double &cs) {
+    const int qlo = (int)((v + (1ull << 50)) >> 51);  // 0..4
+    const double q = (double)qlo;
     double x = fma(-q, c_bm.pio2_hi, t);
     x = fma(-q, c_bm.pio2_lo, x);
     const double z = x * x;
@@ -149,7 +149,7 @@ __device__ __forceinline__ void box_muller_fast(uint4 w, double &z0, double &z1,
     const uint64_t u2 = (((uint64_t)w.w << 32) | w.z) >> 11;
     const double r = bm_sqrt(bm_m2log((1ull << 53) - u, tab));
     double s, c;
-    sincos_2pi(c_bm.two_pi_2m53 * u64_to_f64_xu(u2), s, c);
+    sincos_2pi(c_bm.two_pi_2m53 * u64_to_f64_xu(u2), u2, s, c);
     z0 = __dmul_rn(r, c);
     z1 = __dmul_rn(r, s);
 }

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
     // before the stores.
     const uint64_t n_full = a.n_units / TILE;
     // Box-Muller's log table, staged once per CTA (cbrng_bm.cuh)
-    __shared__ double4 s_bm[OUT == OUT_NORMAL ? 128 : 1];
+    __shared__ double4 s_bm[OUT == OUT_NORMAL ? BM_LOGTAB_N : 1];
     if constexpr (OUT == OUT_NORMAL) bm_stage_table(s_bm);
     for (uint64_t t = warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
 // one thread walks the chain. Latency-bound (~12 dependent ALU ops per word).
 template <int OUT>
 __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1, uint32_t *state_out, uint32_t z) {
-    __shared__ double4 s_bm[OUT == OUT_NORMAL ? 128 : 1];
+    __shared__ double4 s_bm[OUT == OUT_NORMAL ? BM_LOGTAB_N : 1];
     if constexpr (OUT == OUT_NORMAL) bm_stage_table(s_bm);
     uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
     for (uint64_t i = 0; i < n; i++) {
@@ -152,7 +152,7 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
 // with scripted generators, test_distributions.py:29-40, 178-186).
 __global__ void __launch_bounds__(256) normal2_words_kernel(const uint4 *__restrict__ w, uint64_t n_pairs,
                                                             double *__restrict__ z0, double *__restrict__ z1) {
-    __shared__ double4 s_bm[128];
+    __shared__ double4 s_bm[BM_LOGTAB_N];
     bm_stage_table(s_bm);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pairs;
          i += (uint64_t)gridDim.x * blockDim.x) {
