@@ -224,11 +224,10 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
             if (fill_ilp<ALG, OUT>() == 16) return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV>(a, st);
         }
         if constexpr (OUT == OUT_NORMAL && ALG == PHILOX) {
-            // register cap for the FP64 Box-Muller (CBRNG_BM_MINB: CTAs/SM the
-            // allocator must fit; 0 = unconstrained, 52 registers, 4 CTAs/SM)
+            // register cap for the FP64 Box-Muller (CBRNG_BM_MINB=0|8: CTAs/SM the
+            // allocator must fit; 0 = unconstrained; 5 and 6 spill and were
+            // measured no better, profiles/r1s_tune.md)
             static const int mb = env_knob("CBRNG_BM_MINB", BM_MINB_DEFAULT, 0, 8);
-            if (mb == 5) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, 5>(a, st);
-            if (mb == 6) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, 6>(a, st);
             if (mb == 8) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, 8>(a, st);
         }
         return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);

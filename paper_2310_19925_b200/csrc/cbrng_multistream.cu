@@ -236,7 +236,7 @@ constexpr int TY_CH_DEFAULT = 4;
 
 template <int ALG, int OUT, int CV>
 static int launch_staged_cv(const PrefixArgs &a, cudaStream_t st) {
-    if constexpr (ALG == TYCHE) {
+    if constexpr (ALG == TYCHE && OUT == 1) {  // (the u32 variant spills at CH 8)
         static const int ch = [] {
             const char *e = getenv("CBRNG_TY_CH");
             return e ? atoi(e) : TY_CH_DEFAULT;
