@@ -360,6 +360,22 @@ class TestBrownian:
         assert got.tobytes() == want.tobytes()
         assert str(brownian.checksum(p)) == f"{oracle.fnv1a64(want.view(np.uint8).ravel()):016x}"
 
+    def test_cfg3_full_size_spot_check(self, cb, oracle):
+        """configs[2] at full size (10M particles x 10k steps, fused): particles are
+        independent, so the oracle replays 24 pids spread over the range (both
+        ends included) for all 10k steps and must match bit for bit."""
+        n, steps = 10_000_000, 10_000
+        cfg = cb.SimConfig(n, steps)
+        p = cb.init_particles(cfg)
+        cb.brownian.run_steps(p, cfg)
+        rng = np.random.default_rng(3)
+        pids = np.unique(np.concatenate([[0, 1, n // 2, n - 2, n - 1], rng.integers(0, n, 19)])).astype(np.uint64)
+        ref = oracle.brownian_init("philox", pids.size, 0, pid=pids)
+        oracle.brownian_steps("philox", ref, 1, steps, pid=pids)
+        idx = pids.astype(np.int64)
+        for got, r in zip((p.x, p.y, p.vx, p.vy), ref):
+            assert np.array_equal(host(got)[idx], r)
+
     def test_checksum_rejects_unsorted_pids(self, cb):
         import torch
         from paper_2310_19925_b200 import brownian
