@@ -34,13 +34,18 @@ METRIC = "Gsamples/s & HBM GB/s per generator; Brownian-walk particle-steps/s vs
 ALGS = ["philox", "threefry", "squares", "tyche"]
 N_PER_GPU = 1 << 30            # configs[1]: 2^30 f32 values per generator per GPU
 TYCHE_STREAMS, TYCHE_WORDS = 1 << 22, 256
-# ALU-pipe (LOP3/SHF/IADD3/I2FP) instructions per output word of the ALU-bound
-# fills, counted in the SASS main loop (tools/sass_mix.py)
-ALU_OPS_PER_WORD = {
-    "threefry": (20.0, "per 4-word block: 37 SHF.L.W rotations + 39 LOP3 xors + 4 SHF.R (f32 map)"),
-    "tyche": (9.0, "per word: 4 SHF.L.W rotations + 4 LOP3 xors + 1 SHF.R (f32 map); stream warm-up excluded"),
+# INT-pipe work per output word of each headline fill, counted in the SASS main
+# loop of the default kernel (tools/sass_pipes.py): ALU-pipe instructions
+# (LOP3/SHF/IADD3/LEA/ISETP/...) or FMA-heavy slots (IMAD 1, IMAD.HI 2,
+# IMAD.WIDE 2.5 — the measured rates, profiles/r1s_probe_pipes.json). The
+# binding pipe is the one with more work per word.
+INT_WORK_PER_WORD = {
+    "philox": ("fma_heavy", 10.28, "16 IMAD.WIDE (x2.5) + 1 IMAD per 4-word block; ALU 5.6/word"),
+    "threefry": ("alu", 20.19, "37 SHF.L.W + 39 LOP3 + 4 SHF.R per 4-word block; FMA-heavy 14.9 slots/word"),
+    "squares": ("fma_heavy", 14.14, "3 IMAD.WIDE (x2.5) + IMAD.HI (x2) + 4 IMAD per word; ALU 10.1/word"),
+    "tyche": ("alu", 10.92, "4 SHF.L.W + 4 LOP3 + 1 SHF.R per word + staging/addressing + 240-op warm-up per 256-word row"),
 }
-ALU_LANES_PER_CLK_SM = 63.3  # measured LOP3 / SHF.L.W rate, profiles/r1s_probe_pipes.json
+PIPE_LANES_PER_CLK_SM = {"alu": 63.3, "fma_heavy": 63.2}  # measured LOP3 / IMAD rates, profiles/r1s_probe_pipes.json
 
 
 def peaks() -> dict:
@@ -291,21 +296,23 @@ def main() -> None:
         n = per_gen[dom]["ncu"]
         roofline["compute_roofline"] = {"pipe": n["binding_pipe"], "utilization_pct": n.get(n["binding_pipe"]),
                                         "source": n["source"]}
-    if dom in ALU_OPS_PER_WORD:
-        # live ALU-pipe roofline of the dominant kernel: its ALU-pipe instructions
-        # per output word (fixed by the algorithm and the kernel's pipe placement,
-        # DESIGN.md §3) over the measured per-SM ALU rate at the measured clock
-        ops, how = ALU_OPS_PER_WORD[dom]
-        sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz") or 1965.0
-        achieved = ops * N_PER_GPU / (per_gen[dom]["ms"] / 1e3)
-        peak = ALU_LANES_PER_CLK_SM * sms * mhz * 1e6
-        roofline.setdefault("compute_roofline", {}).update({
-            "pipe": "alu", "ops_per_word": ops, "ops_source": how,
-            "achieved_gops": round(achieved / 1e9, 1), "peak_gops": round(peak / 1e9, 1),
-            "frac": round(achieved / peak, 3),
-            "peak_source": f"{ALU_LANES_PER_CLK_SM} ALU thread-ops/clk/SM (profiles/r1s_probe_pipes.json) x {sms} SMs "
-                           f"x {mhz:.0f} MHz (median SM clock in the timed region)"})
+    # INT-pipe roofline per generator (live: words/s over the measured pipe rate
+    # at the measured clock) and the fraction of the slower of the HBM-write and
+    # INT-pipe rooflines (the larger of the two utilisations)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz") or 1965.0
+    for a, (pipe, ops, how) in INT_WORK_PER_WORD.items():
+        achieved = ops * N_PER_GPU / (per_gen[a]["ms"] / 1e3)
+        peak = PIPE_LANES_PER_CLK_SM[pipe] * sms * mhz * 1e6
+        per_gen[a]["int_roofline"] = {"pipe": pipe, "ops_per_word": ops, "frac": round(achieved / peak, 3)}
+        per_gen[a]["binding_frac"] = round(max(per_gen[a]["hbm_frac"], achieved / peak), 3)
+        if a == dom:
+            roofline.setdefault("compute_roofline", {}).update({
+                "pipe": pipe, "ops_per_word": ops, "ops_source": how,
+                "achieved_gops": round(achieved / 1e9, 1), "peak_gops": round(peak / 1e9, 1),
+                "frac": round(achieved / peak, 3),
+                "peak_source": f"{PIPE_LANES_PER_CLK_SM[pipe]} thread-ops/clk/SM (profiles/r1s_probe_pipes.json) "
+                               f"x {sms} SMs x {mhz:.0f} MHz (median SM clock in the timed region)"})
 
     line = {"metric": METRIC, "value": round(value, 3), "unit": "Gsamples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
