@@ -219,14 +219,29 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_k
     }
 }
 
+// Grid: Tyche uses the resident x8 persistent grid like the fills; the
+// counter-based row generators one CTA per 256 streams (every thread one row):
+// Philox 1e8 x 256 words 5386 -> 5689 GB/s (profiles/r1t_tune.md).
+template <int ALG>
+static unsigned staged_grid(uint64_t n_streams) {
+    const uint64_t work = (n_streams + 255) / 256;
+    if constexpr (ALG == TYCHE) {
+        return 0;  // caller uses grid_for
+    } else {
+        return (unsigned)(work < 0x7FFFFFFFull ? work : 0x7FFFFFFFull);
+    }
+}
+
 template <int ALG, int OUT, int CV, int CH>
 static int launch_staged_ch(const PrefixArgs &a, cudaStream_t st) {
     if (a.nwords % 4 == 0) {
         auto k = staged_prefix_kernel<ALG, OUT, true, CV, CH>;
-        k<<<grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
+        const unsigned g = staged_grid<ALG>(a.n_streams);
+        k<<<g ? g : grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
     } else {
         auto k = staged_prefix_kernel<ALG, OUT, false, CV, CH>;
-        k<<<grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
+        const unsigned g = staged_grid<ALG>(a.n_streams);
+        k<<<g ? g : grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
     }
     return check_launch("staged_prefix_kernel");
 }
