@@ -36,6 +36,7 @@ struct BrownArgs {
     double gm, dt, sqrt_dt;
     double kick_scale;  // sqrt_dt * 2^-52 (see kick())
     int fold;           // kick_scale is exact and normal: use the folded kick
+    int reverse;        // per-step launches alternate the particle order (L2 reuse)
 };
 
 // Per-particle, step-invariant state.
@@ -153,7 +154,10 @@ __device__ __forceinline__ void step_update(double &x, double &y, double &vx, do
 // spill) 3.27e11 (profiles/r1j_tune.md).
 template <int ALG, bool HI0, bool FOLD, int MINB>
 __global__ void __launch_bounds__(256, MINB) brownian_steps_kernel(const __grid_constant__ BrownArgs a) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (uint64_t)gridDim.x * blockDim.x) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += (uint64_t)gridDim.x * blockDim.x) {
+        // per-step mode walks the arrays in alternating directions, so each step
+        // starts on the particles the previous step wrote last — still in L2
+        const uint64_t i = a.reverse ? a.n - 1 - j : j;
         const uint64_t pid = a.pid ? a.pid[i] : a.pid_base + i;
         double x = a.x[i], y = a.y[i], vx = a.vx[i], vy = a.vy[i];
         const Particle<ALG, HI0> P(pid);
@@ -247,6 +251,15 @@ __global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint
     }
 }
 
+// CBRNG_BROWNIAN_PINGPONG=0 keeps every per-step launch in ascending order (A/B runs).
+static bool brownian_pingpong() {
+    static const bool v = [] {
+        const char *e = getenv("CBRNG_BROWNIAN_PINGPONG");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return v;
+}
+
 // MINB applies to the fused table kernel; the per-step kernel keeps 5 CTAs/SM
 // (6 spills there).
 template <int ALG, bool HI0, bool FOLD, int MINB>
@@ -266,6 +279,7 @@ static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
     const uint64_t per_launch = mode == CBRNG_BROWNIAN_FUSED ? 0xFFFFFFFFull : 1;
     for (uint64_t done = 0; done < total;) {
         a.nsteps = total - done < per_launch ? total - done : per_launch;
+        a.reverse = mode == CBRNG_BROWNIAN_PER_STEP && brownian_pingpong() ? (int)(a.first_it & 1) : 0;
         k<<<grid, 256, 0, st>>>(a);
         a.first_it += a.nsteps;
         done += a.nsteps;
@@ -350,7 +364,7 @@ int cbrng_brownian_init(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_b
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(x && y && vx && vy, "NULL particle array");
-    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, 0, 0, 0.0, 0.0, 0.0, 0.0, 0};
+    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, 0, 0, 0.0, 0.0, 0.0, 0.0, 0, 0};
     cudaStream_t st = as_stream(stream);
     const unsigned grid = (unsigned)((n + 255) / 256);
     switch (alg) {
@@ -373,7 +387,7 @@ int cbrng_brownian_steps(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_
     if (n == 0 || nsteps == 0) return CBRNG_OK;
     CBRNG_REQUIRE(x && y && vx && vy, "NULL particle array");
     // Host-side scalars exactly as the reference forms them (brownian.py:134, :177).
-    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, first_it, nsteps, gamma / mass, dt, std::sqrt(dt), 0.0, 0};
+    BrownArgs a{n, pid, pid_base, x, y, vx, vy, init_ctr, first_it, nsteps, gamma / mass, dt, std::sqrt(dt), 0.0, 0, 0};
     a.kick_scale = a.sqrt_dt * 0x1p-52;
     // fold only when the scaled constant is exact (normal, no underflow)
     a.fold = a.sqrt_dt == 0.0 || (a.kick_scale >= 0x1p-1022 && a.kick_scale * 0x1p52 == a.sqrt_dt);

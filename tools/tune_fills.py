@@ -50,6 +50,9 @@ p = brownian.init_particles(cfg)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 brownian.run_steps(p, cfg); e0.record(); brownian.run_steps(p, cfg, start_iteration=201); e1.record(); e1.synchronize()
 res["brownian_fused_psteps"] = {"gbs": round(10_000_000 * 200 / (e0.elapsed_time(e1) / 1e3) / 1e9, 1)}
+cps = brownian.SimConfig(10_000_000, 100, mode="per_step")
+brownian.run_steps(p, cps, start_iteration=401); e0.record(); brownian.run_steps(p, cps, start_iteration=501); e1.record(); e1.synchronize()
+res["brownian_per_step_psteps"] = {"gbs": round(10_000_000 * 100 / (e0.elapsed_time(e1) / 1e3) / 1e9, 1)}
 print(json.dumps(res))
 '''
 
