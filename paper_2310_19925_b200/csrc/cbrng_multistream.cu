@@ -11,6 +11,7 @@
 //   * shorter rows: lanes map to contiguous 16-byte chunks of consecutive rows
 //     (prefix_kernel).
 #include <cstdlib>
+#include <type_traits>
 
 #include "cbrng_internal.cuh"
 
@@ -164,7 +165,10 @@ template <int ALG> constexpr int staged_min_blocks() { return ALG == TYCHE ? 8 :
 
 // CH: 16-byte chunks staged per row per round: 4 (64 B of each row per store
 // instruction, 8 rows; 16 KB/CTA) or 8 (full 128 B lines, 4 rows; 32 KB/CTA).
-template <int ALG, int OUT, bool VEC, int CV, int CH = 4>
+// NW: the row length when known at compile time (256: configs[1]'s Tyche rows
+// and configs[4]); a full warp's copy-out then stores through one pointer with
+// immediate row offsets and no per-row predicates.
+template <int ALG, int OUT, bool VEC, int CV, int CH = 4, int NW = 0>
 __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_kernel(const __grid_constant__ PrefixArgs a) {
     static_assert(CH == 4 || CH == 8, "CH");
     constexpr uint32_t RPI = 32 / CH;  // rows per copy-out instruction
@@ -189,6 +193,27 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_k
         uint64_t at = (s0 + rrow) * a.nwords + rc * 4;
         const uint64_t rstride = (uint64_t)RPI * a.nwords;
         const uint32_t rows_left = a.n_streams - s0 < 32 ? (uint32_t)(a.n_streams - s0) : 32u;
+        if constexpr (NW != 0 && VEC && CH == 4) {
+            if (rows_left == 32) {
+                // full warp, compile-time row length: rows rrow + 8k sit at
+                // immediate offsets k * 8 * NW words from one pointer
+                using V4 = typename std::conditional<OUT == 0, uint4, float4>::type;
+                V4 *ptr = reinterpret_cast<V4 *>(a.out) + at / 4;
+                for (uint32_t g = 0; g < (uint32_t)NW / 16; g++, ptr += 4) {
+#pragma unroll
+                    for (int c = 0; c < CH; c++) my[lane * CH + (c ^ wx)] = gen.next4();
+                    __syncwarp();
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const uint4 v = my[rslot + 32 * k];
+                        if constexpr (OUT == 0) __stcs(reinterpret_cast<uint4 *>(ptr) + k * 2 * NW, v);
+                        else __stcs(reinterpret_cast<float4 *>(ptr) + k * 2 * NW, u32x4_to_f32x4<CV>(v, a.m24));
+                    }
+                    __syncwarp();
+                }
+                continue;
+            }
+        }
         for (uint32_t g = 0; g < groups; g++, at += 4 * CH) {
 #pragma unroll
             for (int c = 0; c < CH; c++) my[lane * CH + (c ^ wx)] = gen.next4();
@@ -222,26 +247,48 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_k
 // Grid: Tyche uses the resident x8 persistent grid like the fills; the
 // counter-based row generators one CTA per 256 streams (every thread one row):
 // Philox 1e8 x 256 words 5386 -> 5689 GB/s (profiles/r1t_tune.md).
+// f32 conversion placement per generator (B200 sweeps, profiles/r1r_tune.md,
+// r1t_tune.md); CBRNG_CVT_MS=0..5 overrides for tuning runs. Tyche's lean
+// 256-word copy-out prefers the shift on the multiplier (IMAD.HI) and I2FP.
+template <int ALG> constexpr int ms_cv_default() { return ALG == SQUARES ? 0 : ALG == TYCHE ? 1 : 4; }
+
+// Tyche: CBRNG_TY_GRID = k -> k x resident CTAs (persistent), 0 -> one CTA per
+// 256 streams.
+constexpr int TY_GRID_DEFAULT = 8;
+
 template <int ALG>
-static unsigned staged_grid(uint64_t n_streams) {
+static unsigned staged_grid(const void *kernel, uint64_t n_streams) {
     const uint64_t work = (n_streams + 255) / 256;
     if constexpr (ALG == TYCHE) {
-        return 0;  // caller uses grid_for
+        static const int k = [] {
+            const char *e = getenv("CBRNG_TY_GRID");
+            return e ? atoi(e) : TY_GRID_DEFAULT;
+        }();
+        if (k > 0) {
+            const uint64_t g = (uint64_t)resident_blocks(kernel, 256, 0) * k;
+            return (unsigned)(g < work ? g : work);
+        }
     } else {
-        return (unsigned)(work < 0x7FFFFFFFull ? work : 0x7FFFFFFFull);
+        (void)kernel;
     }
+    return (unsigned)(work < 0x7FFFFFFFull ? work : 0x7FFFFFFFull);
 }
 
 template <int ALG, int OUT, int CV, int CH>
 static int launch_staged_ch(const PrefixArgs &a, cudaStream_t st) {
+    if constexpr (CH == 4 && ALG != THREEFRY) {  // (Threefry's folded schedule spills with it)
+        if (a.nwords == 256) {
+            auto k = staged_prefix_kernel<ALG, OUT, true, CV, CH, 256>;
+            k<<<staged_grid<ALG>(reinterpret_cast<const void *>(k), a.n_streams), 256, 0, st>>>(a);
+            return check_launch("staged_prefix_kernel");
+        }
+    }
     if (a.nwords % 4 == 0) {
         auto k = staged_prefix_kernel<ALG, OUT, true, CV, CH>;
-        const unsigned g = staged_grid<ALG>(a.n_streams);
-        k<<<g ? g : grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
+        k<<<staged_grid<ALG>(reinterpret_cast<const void *>(k), a.n_streams), 256, 0, st>>>(a);
     } else {
         auto k = staged_prefix_kernel<ALG, OUT, false, CV, CH>;
-        const unsigned g = staged_grid<ALG>(a.n_streams);
-        k<<<g ? g : grid_for(k, 256, 0, (a.n_streams + 255) / 256), 256, 0, st>>>(a);
+        k<<<staged_grid<ALG>(reinterpret_cast<const void *>(k), a.n_streams), 256, 0, st>>>(a);
     }
     return check_launch("staged_prefix_kernel");
 }
@@ -261,9 +308,6 @@ static int launch_staged_cv(const PrefixArgs &a, cudaStream_t st) {
     return launch_staged_ch<ALG, OUT, CV, 4>(a, st);
 }
 
-// f32 conversion placement per generator (B200 sweep, profiles/r1r_tune.md);
-// CBRNG_CVT_MS=0..5 overrides for tuning runs.
-template <int ALG> constexpr int ms_cv_default() { return ALG == SQUARES ? 0 : 4; }
 
 template <int ALG, int OUT>
 static int launch_staged(const PrefixArgs &a, cudaStream_t st) {

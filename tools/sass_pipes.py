@@ -58,12 +58,13 @@ def main() -> None:
     print("philox  ", pipes(mix(FILL, "_ZN5cbrng11fill_kernelILi0ELi1ELi16ELb0ELi0ELi4ELi0EEEvNS_8FillArgsIXT_EEE"), 64))
     print("threefry", pipes(mix(FILL, "_ZN5cbrng11fill_kernelILi1ELi1ELi8ELb0ELi4ELi4ELi0EEEvNS_8FillArgsIXT_EEE"), 32))
     print("squares ", pipes(mix(FILL, "_ZN5cbrng11fill_kernelILi2ELi1ELi8ELb0ELi1ELi0ELi0EEEvNS_8FillArgsIXT_EEE"), 32))
-    ty = "_ZN5cbrng20staged_prefix_kernelILi3ELi1ELb1ELi4ELi4EEEvNS_10PrefixArgsE"
-    # Tyche: the 16-word staging group loop, plus the per-row work (warm-up,
-    # first group, setup) spread over a 256-word row. Addresses of the build
-    # this was read from (r1v); re-read them from `cuobjdump -sass` after changes.
-    print("tyche group", pipes(mix(MULTI, ty, 0x1BF0, 0x2EC0), 16))
-    print("tyche row  ", pipes(mix(MULTI, ty, 0x1F0, 0x1BEF), 256))
+    ty = "_ZN5cbrng20staged_prefix_kernelILi3ELi1ELb1ELi1ELi4ELi256EEEvNS_10PrefixArgsE"
+    # Tyche (256-word rows, CV 1): the full-warp 16-word staging loop, plus the
+    # per-row warm-up (tyche_init: a 4-mix loop body run 5 times) spread over the
+    # row. Addresses of the build this was read from (r1w); re-read them from
+    # `cuobjdump -sass` after changes.
+    print("tyche group ", pipes(mix(MULTI, ty, 0x35F0, 0x4660), 16))
+    print("tyche warmup", pipes(mix(MULTI, ty, 0x440, 0x760), 256 / 5))
 
 
 if __name__ == "__main__":
