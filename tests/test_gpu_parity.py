@@ -266,9 +266,13 @@ class TestPrefixWords:
     def test_row_shapes(self, cb, oracle, alg):
         from paper_2310_19925_b200 import bulk
 
-        for n, nw in ((1, 1), (33, 8), (100, 36), (65, 128), (7, 260), (1000, 33)):
+        # incl. 256-word rows (the compile-time-specialised kernel) with full and
+        # partial warps of streams
+        for n, nw in ((1, 1), (33, 8), (100, 36), (65, 128), (7, 260), (1000, 33), (1000, 256), (5, 256), (64, 256)):
             got = host(bulk.prefix_words(alg, range(1000, 1000 + n), 3, nw))
             assert np.array_equal(got, oracle.prefix_words_arange(alg, 1000, n, 3, nw))
+            f = host(bulk.prefix_uniform_f32(alg, range(1000, 1000 + n), 3, nw)).reshape(-1)
+            assert np.array_equal(f, oracle.words_to_f32(oracle.prefix_words_arange(alg, 1000, n, 3, nw)))
 
     @pytest.mark.parametrize("alg", ALGS)
     def test_prefix_uniform_f32(self, cb, oracle, alg):
