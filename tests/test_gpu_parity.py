@@ -642,3 +642,42 @@ class TestHostPipelinedFills:
         got = bulk.prefix_uniform_f32("philox", seeds, 0, nw, device="cpu")
         assert isinstance(got, np.ndarray) and got.shape == (n, nw)
         assert np.array_equal(got, host(bulk.prefix_uniform_f32("philox", seeds, 0, nw)))
+
+
+class TestReentrancy:
+    """The C ABI is reentrant (no global mutable state but thread-safe launch
+    caches; thread-local error text), as the reference's nogil numba kernels are
+    called from a thread pool (brownian.py:185-191): concurrent calls from
+    several host threads, each on its own CUDA stream, give the sequential results."""
+
+    def test_concurrent_fills_and_errors(self, cb, oracle):
+        import threading
+
+        import torch
+
+        from paper_2310_19925_b200 import _lib
+
+        lib = _lib.lib()
+        n = 1 << 20
+        jobs = [(a, s) for a in range(3) for s in range(4)]
+        outs = {j: torch.empty(n, dtype=torch.uint32, device="cuda") for j in jobs}
+        errs = {}
+
+        def work(j):
+            a, s = j
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                rc = lib.cbrng_words(a, 1000 + s, s, 0, None, n, outs[j].data_ptr(), None, int(st.cuda_stream))
+                bad = lib.cbrng_words(9, 0, 0, 0, None, 1, outs[j].data_ptr(), None, int(st.cuda_stream))
+                errs[j] = (rc, bad, lib.cbrng_last_error().decode())
+            st.synchronize()
+
+        threads = [threading.Thread(target=work, args=(j,)) for j in jobs]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        names = ["philox", "threefry", "squares"]
+        for (a, s), (rc, bad, msg) in errs.items():
+            assert rc == 0 and bad == _lib.CBRNG_EALG and "algorithm" in msg
+            assert np.array_equal(host(outs[(a, s)]), oracle.stream_words(names[a], 1000 + s, s, n))
