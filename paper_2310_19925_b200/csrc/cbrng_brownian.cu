@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(256, MINB) brownian_fused_philox_kernel(const 
         for (uint32_t j = threadIdx.x; j < BR_TAB; j += blockDim.x) tab[j] = philox_step_uniform(ctr0 + base + j);
         __syncthreads();
         const uint32_t m = nsteps - base < (uint32_t)BR_TAB ? nsteps - base : (uint32_t)BR_TAB;
+#pragma unroll 2  // steps s and s+1 interleave (the cipher of s+1 under the FP64 chain of s): +3.5 %, r1t_tune.md
         for (uint32_t s = 0; s < m; s++) step_update<FOLD>(x, y, vx, vy, philox_particle_block_u(P, tab[s]), a);
     }
     if (live) { a.x[i] = x; a.y[i] = y; a.vx[i] = vx; a.vy[i] = vy; }
@@ -287,20 +288,16 @@ static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
     return check_launch("brownian_steps_kernel");
 }
 
-constexpr int BROWNIAN_MINB_DEFAULT = 5;
+constexpr int BROWNIAN_MINB = 5;
 
 template <int ALG, bool HI0, bool FOLD>
 static int launch_steps_k(BrownArgs a, int mode, cudaStream_t st) {
     if constexpr (!HI0) {
         return launch_steps_kb<ALG, HI0, FOLD, 1>(a, mode, st);  // 64-bit pids: 20 live keys, no cap
     } else {
-        // register cap (CTAs/SM), CBRNG_BROWNIAN_MINB=5|6 overrides for tuning runs
-        static const int mb = [] {
-            const char *e = getenv("CBRNG_BROWNIAN_MINB");
-            return e ? atoi(e) : BROWNIAN_MINB_DEFAULT;
-        }();
-        if (mb == 6) return launch_steps_kb<ALG, HI0, FOLD, 6>(a, mode, st);
-        return launch_steps_kb<ALG, HI0, FOLD, 5>(a, mode, st);
+        // register cap: 5 CTAs/SM (6 measured no better and spills with the
+        // unrolled step loop, r1t_tune.md)
+        return launch_steps_kb<ALG, HI0, FOLD, BROWNIAN_MINB>(a, mode, st);
     }
 }
 
