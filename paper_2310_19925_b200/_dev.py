@@ -127,21 +127,24 @@ def pipelined_host_fill(n: int, dtype: torch.dtype, hosts: list, launch, row: in
     copy = torch.cuda.Stream(dev)
     bufs = [[torch.empty(k * row, dtype=dtype, device=dev) for _ in hosts] for _ in range(2)]
     copied = [None, None]
-    for i, off in enumerate(range(0, n, k)):
-        slot, m = i & 1, min(k, n - off)
-        if copied[slot] is not None:
-            comp.wait_event(copied[slot])  # the slot's previous chunk has left the GPU
-        launch([b.data_ptr() for b in bufs[slot]], off, m, int(comp.cuda_stream))
-        ready = torch.cuda.Event()
-        ready.record(comp)
-        copy.wait_event(ready)
-        with torch.cuda.stream(copy):
-            for h, b in zip(hosts, bufs[slot]):
-                h[off * row:(off + m) * row].copy_(b[:m * row], non_blocking=True)
-        done = torch.cuda.Event()
-        done.record(copy)
-        copied[slot] = done
-    copy.synchronize()
+    try:
+        for i, off in enumerate(range(0, n, k)):
+            slot, m = i & 1, min(k, n - off)
+            if copied[slot] is not None:
+                comp.wait_event(copied[slot])  # the slot's previous chunk has left the GPU
+            launch([b.data_ptr() for b in bufs[slot]], off, m, int(comp.cuda_stream))
+            ready = torch.cuda.Event()
+            ready.record(comp)
+            copy.wait_event(ready)
+            with torch.cuda.stream(copy):
+                for h, b in zip(hosts, bufs[slot]):
+                    h[off * row:(off + m) * row].copy_(b[:m * row], non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(copy)
+            copied[slot] = done
+    finally:
+        # also on error: no copy may still read a device buffer once it is freed
+        copy.synchronize()
 
 
 def to_numpy(x) -> np.ndarray:
