@@ -203,7 +203,7 @@ static int fill_ilp() {
 // generator. CBRNG_TF_VARIANT=0..8 and CBRNG_CVT=0..5 override for tuning runs.
 constexpr int TF_V_DEFAULT = 4;
 constexpr int BM_MINB_DEFAULT = 8;  // r1s sweep: 0 -> 8 = +4 % (profiles/r1s_tune.md)
-template <int ALG> constexpr int cv_default() { return ALG == SQUARES ? 0 : 4; }
+template <int ALG> constexpr int cv_default() { return 4; }  // all three fills: SHF + I2F (XU) + FMUL
 
 static int tf_variant() {
     static int v = env_knob("CBRNG_TF_VARIANT", TF_V_DEFAULT, 0, 8);
