@@ -154,13 +154,20 @@ __device__ __forceinline__ void step_update(double &x, double &y, double &vx, do
 // spill) 3.27e11 (profiles/r1j_tune.md).
 template <int ALG, bool HI0, bool FOLD, int MINB>
 __global__ void __launch_bounds__(256, MINB) brownian_steps_kernel(const __grid_constant__ BrownArgs a) {
+    // Programmatic dependent launch (per-step mode): once every CTA of this grid
+    // has started, the next step's grid may be scheduled onto the SMs this
+    // grid's tail leaves idle; it sets up its particles' key schedules and waits
+    // (griddepcontrol.wait) for this grid's writes before reading the state.
+    // Both are no-ops for a normally launched grid.
+    asm volatile("griddepcontrol.launch_dependents;");
     for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < a.n; j += (uint64_t)gridDim.x * blockDim.x) {
         // per-step mode walks the arrays in alternating directions, so each step
         // starts on the particles the previous step wrote last — still in L2
         const uint64_t i = a.reverse ? a.n - 1 - j : j;
         const uint64_t pid = a.pid ? a.pid[i] : a.pid_base + i;
-        double x = a.x[i], y = a.y[i], vx = a.vx[i], vy = a.vy[i];
         const Particle<ALG, HI0> P(pid);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        double x = a.x[i], y = a.y[i], vx = a.vx[i], vy = a.vy[i];
         uint32_t ctr = a.init_ctr + (uint32_t)a.first_it;
         const uint32_t nsteps = (uint32_t)a.nsteps;  // host splits launches at 2^32 - 1 steps
         for (uint32_t s = 0; s < nsteps; s++, ctr++) step_update<FOLD>(x, y, vx, vy, P.words(ctr), a);
@@ -261,6 +268,16 @@ static bool brownian_pingpong() {
     return v;
 }
 
+// CBRNG_BROWNIAN_PDL=0 launches the per-step grids without programmatic
+// dependent launch (A/B runs).
+static bool brownian_pdl() {
+    static const bool v = [] {
+        const char *e = getenv("CBRNG_BROWNIAN_PDL");
+        return e ? atoi(e) != 0 : true;
+    }();
+    return v;
+}
+
 // MINB applies to the fused table kernel; the per-step kernel keeps 5 CTAs/SM
 // (6 spills there).
 template <int ALG, bool HI0, bool FOLD, int MINB>
@@ -281,7 +298,21 @@ static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
     for (uint64_t done = 0; done < total;) {
         a.nsteps = total - done < per_launch ? total - done : per_launch;
         a.reverse = mode == CBRNG_BROWNIAN_PER_STEP && brownian_pingpong() ? (int)(a.first_it & 1) : 0;
-        k<<<grid, 256, 0, st>>>(a);
+        if (mode == CBRNG_BROWNIAN_PER_STEP && brownian_pdl()) {
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(256);
+            cfg.stream = st;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            const int rc = check_cuda(cudaLaunchKernelEx(&cfg, k, a), "cudaLaunchKernelEx");
+            if (rc) return rc;
+        } else {
+            k<<<grid, 256, 0, st>>>(a);
+        }
         a.first_it += a.nsteps;
         done += a.nsteps;
     }
