@@ -13,6 +13,9 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "cbrng_internal.cuh"
 
 namespace cbrng {
@@ -247,14 +250,90 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_k
 // Grid: Tyche uses the resident x8 persistent grid like the fills; the
 // counter-based row generators one CTA per 256 streams (every thread one row):
 // Philox 1e8 x 256 words 5386 -> 5689 GB/s (profiles/r1t_tune.md).
+// 256-word rows with the copy-out done by the tensor-memory accelerator: the
+// warp stages its 32 rows x 16 words in shared memory exactly as
+// staged_prefix_kernel does (16-byte chunk c of row r at c ^ ((r >> 1) & 3),
+// which is the hardware's SWIZZLE_64B pattern for 64-byte rows), then one lane
+// issues a single 2 KB cp.async.bulk.tensor store of the [32 x 16] box. No
+// LDS/STG per lane, no row predicates: the TMA clips rows past n_streams.
+// The f32 map is applied before staging.
+template <int ALG, int OUT, int CV>
+__global__ void __launch_bounds__(256, staged_min_blocks<ALG>())
+    staged_tma_kernel(const __grid_constant__ PrefixArgs a, const __grid_constant__ CUtensorMap tmap) {
+    __shared__ __align__(1024) uint4 tile[TY_WARPS][32 * 4];
+    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint4 *const my = tile[wib];
+    const uint32_t smem = (uint32_t)__cvta_generic_to_shared(my);
+    const uint32_t wx = (lane >> 1) & 3;
+    for (uint64_t s0 = warp * 32; s0 < a.n_streams; s0 += nwarps * 32) {
+        const uint64_t sid = s0 + lane;
+        const bool valid = sid < a.n_streams;
+        RowGen<ALG> gen(valid ? seed_of(a, sid) : 0, valid ? ctr_of(a, sid) : 0);
+        for (uint32_t g = 0; g < a.nwords / 16; g++) {
+            // the previous store of this warp's tile must have read it
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                uint4 w = gen.next4();
+                if constexpr (OUT == 1) {
+                    const float4 f = u32x4_to_f32x4<CV>(w, a.m24);
+                    w = make_uint4(__float_as_uint(f.x), __float_as_uint(f.y), __float_as_uint(f.z), __float_as_uint(f.w));
+                }
+                my[lane * 4 + (c ^ wx)] = w;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> TMA
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n\t"
+                    "cp.async.bulk.commit_group;"
+                    :
+                    : "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((int)(16 * g)), "r"((int)s0), "r"(smem)
+                    : "memory");
+            }
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// [n_streams][nwords] 4-byte elements, box 32 rows x 16 words, 64-byte swizzle.
+static bool rows_tensor_map(CUtensorMap *m, void *out, uint64_t n_streams, uint32_t nwords, bool f32) {
+    const auto encode = tensor_map_encoder();
+    if (!encode || n_streams > 0x7FFFFFFFull) return false;
+    const cuuint64_t dims[2] = {nwords, n_streams};
+    const cuuint64_t strides[1] = {(cuuint64_t)nwords * 4};
+    const cuuint32_t box[2] = {16, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // f32 conversion placement per generator (B200 sweeps, profiles/r1r_tune.md,
 // r1t_tune.md); CBRNG_CVT_MS=0..5 overrides for tuning runs. Tyche's lean
 // 256-word copy-out prefers the shift on the multiplier (IMAD.HI) and I2FP.
 template <int ALG> constexpr int ms_cv_default() { return ALG == SQUARES ? 0 : ALG == TYCHE ? 1 : 4; }
 
+constexpr bool MS_TMA_DEFAULT = false;
+
 // Tyche: CBRNG_TY_GRID = k -> k x resident CTAs (persistent), 0 -> one CTA per
 // 256 streams.
-constexpr int TY_GRID_DEFAULT = 8;
+constexpr int TY_GRID_DEFAULT = 0;  // one CTA per 256 streams: robust across boxes (r1t_tune.md)
 
 template <int ALG>
 static unsigned staged_grid(const void *kernel, uint64_t n_streams) {
@@ -276,6 +355,19 @@ static unsigned staged_grid(const void *kernel, uint64_t n_streams) {
 
 template <int ALG, int OUT, int CV, int CH>
 static int launch_staged_ch(const PrefixArgs &a, cudaStream_t st) {
+    if constexpr (CH == 4 && ALG != THREEFRY) {
+        // TMA copy-out (CBRNG_MS_TMA=0 keeps the LDS/STG copy-out)
+        static const bool tma = [] {
+            const char *e = getenv("CBRNG_MS_TMA");
+            return e ? atoi(e) != 0 : MS_TMA_DEFAULT;
+        }();
+        CUtensorMap m;
+        if (tma && a.nwords == 256 && rows_tensor_map(&m, a.out, a.n_streams, a.nwords, OUT == 1)) {
+            auto k = staged_tma_kernel<ALG, OUT, CV>;
+            k<<<staged_grid<ALG>(reinterpret_cast<const void *>(k), a.n_streams), 256, 0, st>>>(a, m);
+            return check_launch("staged_tma_kernel");
+        }
+    }
     if constexpr (CH == 4 && ALG != THREEFRY) {  // (Threefry's folded schedule spills with it)
         if (a.nwords == 256) {
             auto k = staged_prefix_kernel<ALG, OUT, true, CV, CH, 256>;

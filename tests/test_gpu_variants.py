@@ -75,3 +75,40 @@ def test_ilp_variants(ilp):
 @pytest.mark.parametrize("ch", [4, 8])
 def test_tyche_staging_width(ch):
     assert _run({"CBRNG_TY_CH": str(ch)}) == []
+
+
+CHILD_ROWS256 = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2310_19925_b200 import bulk
+from oracle import oracle as orc
+bad = []
+for alg in ("philox", "threefry", "squares", "tyche"):
+    for n in (5, 64, 1000):
+        ref = orc.prefix_words_arange(alg, 9, n, 2, 256)
+        if not np.array_equal(bulk.prefix_words(alg, range(9, 9 + n), 2, 256).cpu().numpy(), ref):
+            bad.append(["u32", alg, n])
+        got = bulk.prefix_uniform_f32(alg, range(9, 9 + n), 2, 256).cpu().numpy().reshape(-1)
+        if not np.array_equal(got, orc.words_to_f32(ref)):
+            bad.append(["f32", alg, n])
+    seeds = np.arange(333, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    ctrs = np.arange(333, dtype=np.uint32) * np.uint32(7)
+    got = bulk.prefix_words(alg, seeds, ctrs, 256).cpu().numpy()
+    if not np.array_equal(got, orc.prefix_words(alg, seeds, ctrs, 256)):
+        bad.append(["arrays", alg])
+print(json.dumps(bad))
+"""
+
+
+@pytest.mark.parametrize("tma", [0, 1])
+def test_rows256_copy_out(tma):
+    """256-word rows through the LDS/STG copy-out and the TMA-store copy-out."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, CBRNG_MS_TMA=str(tma))
+    r = subprocess.run([sys.executable, "-c", CHILD_ROWS256 % str(ROOT)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1]) == []
