@@ -83,6 +83,58 @@ def apply(g: Generator, op: str, arg: int):
     raise ValueError(op)
 
 
+def bulk_traces(rnd: random.Random) -> list:
+    """Random calls of the multi-stream and vector entry points (bulk.py:49-296)."""
+    from cbrng import bulk
+    from cbrng.generators import Algorithm
+
+    out = []
+    rng = np.random.default_rng(19925)
+    for t in range(48):
+        alg = ALGS[t % 4]
+        a = Algorithm.from_name(alg)
+        n = rnd.choice([1, 2, 31, 32, 33, 257, 1000])
+        nw = rnd.choice([1, 3, 4, 8, 16, 17, 36, 256])
+        seeds = rng.integers(0, 2**64, size=n, dtype=np.uint64)
+        ctrs = rng.integers(0, 2**32, size=n, dtype=np.uint64).astype(np.uint32)
+        scalar_ctr = rnd.random() < 0.5
+        c_arg = int(ctrs[0]) if scalar_ctr else ctrs
+        w = bulk.prefix_words(a, seeds, c_arg, nw)
+        out.append({"call": "prefix_words", "alg": alg, "seeds": [int(x) for x in seeds],
+                    "ctrs": int(ctrs[0]) if scalar_ctr else [int(x) for x in ctrs], "nwords": nw,
+                    "sha": h16(np.ascontiguousarray(w, np.uint32).tobytes())})
+        f = bulk.first_words(a, seeds, c_arg)
+        out.append({"call": "first_words", "alg": alg, "seeds": [int(x) for x in seeds],
+                    "ctrs": int(ctrs[0]) if scalar_ctr else [int(x) for x in ctrs],
+                    "sha": h16(np.ascontiguousarray(f, np.uint32).tobytes())})
+        src = bulk.AlgorithmSource(a)
+        seed, ctr, m = int(seeds[0]), int(ctrs[0]), rnd.choice([1, 5, 129, 5000])
+        out.append({"call": "source_stream_words", "alg": alg, "seed": seed, "ctr": ctr, "n": m,
+                    "sha": h16(np.ascontiguousarray(src.stream_words(seed, ctr, m), np.uint32).tobytes())})
+    v = {k: rng.integers(0, 2**32, size=777, dtype=np.uint64).astype(np.uint32) for k in "abcdefgh"}
+    out.append({"call": "philox4x32", "in": {k: [int(x) for x in v[k]] for k in "abcdef"},
+                "sha": h16(np.stack(bulk.philox4x32(v["a"], v["b"], v["c"], v["d"], v["e"], v["f"])).astype(np.uint32).tobytes())})
+    out.append({"call": "threefry4x32", "in": {k: [int(x) for x in v[k]] for k in "abcdefgh"},
+                "sha": h16(np.stack(bulk.threefry4x32(*(v[k] for k in "abcdefgh"))).astype(np.uint32).tobytes())})
+    s64 = rng.integers(0, 2**64, size=777, dtype=np.uint64)
+    keys = bulk.squares_keys(s64)
+    out.append({"call": "squares_keys", "seeds": [int(x) for x in s64], "sha": h16(np.asarray(keys, np.uint64).tobytes())})
+    c64 = rng.integers(0, 2**64, size=777, dtype=np.uint64)
+    out.append({"call": "squares32", "ctr": [int(x) for x in c64], "key": [int(x) for x in keys],
+                "sha": h16(np.asarray(bulk.squares32(c64, keys), np.uint32).tobytes())})
+    ti = bulk.tyche_init(s64, v["a"])
+    out.append({"call": "tyche_init", "seeds": [int(x) for x in s64], "ctrs": [int(x) for x in v["a"]],
+                "sha": h16(np.stack(ti).astype(np.uint32).tobytes())})
+    tm = bulk.tyche_mix(v["a"], v["b"], v["c"], v["d"])
+    out.append({"call": "tyche_mix", "in": {k: [int(x) for x in v[k]] for k in "abcd"},
+                "sha": h16(np.stack(tm).astype(np.uint32).tobytes())})
+    for steps in (0, 1, 7, 1000):
+        st = (int(v["a"][0]), int(v["b"][0]), int(v["c"][0]), int(v["d"][0]))
+        out.append({"call": "tyche_advance_state", "state": list(st), "steps": steps,
+                    "res": [int(x) for x in bulk.tyche_advance_state(st, steps)]})
+    return out
+
+
 def main() -> None:
     rnd = random.Random(2310_19925)
     traces = []
@@ -107,7 +159,8 @@ def main() -> None:
                 steps.append({"op": op, "arg": arg, "res": res, "state": g.state_bytes().hex()})
             traces.append({"alg": alg, "seed": seed, "ctr": ctr, "steps": steps})
     OUT.write_text(json.dumps({"generator": "tests/golden/make_api_traces.py",
-                               "reference": "cbrng 0.1.0 (/root/reference/pkg/src)", "traces": traces}, indent=0))
+                               "reference": "cbrng 0.1.0 (/root/reference/pkg/src)", "traces": traces,
+                               "bulk": bulk_traces(rnd)}, indent=0))
     print("wrote", OUT, sum(len(t["steps"]) for t in traces), "steps")
 
 

@@ -93,3 +93,50 @@ def test_trace(cb, k):
         else:
             assert res == s["res"], where
         assert g.state_bytes().hex() == s["state"], where
+
+
+BULK = json.loads((Path(__file__).resolve().parent / "golden" / "api_traces.json").read_text())["bulk"]
+
+
+def _sha32(x) -> str:
+    return h16(np.ascontiguousarray(np.asarray(x), np.uint32).tobytes())
+
+
+@pytest.mark.parametrize("k", range(len(BULK)))
+def test_bulk_call(cb, k):
+    """Multi-stream and vector entry points (bulk.py:49-296) on recorded inputs."""
+    from paper_2310_19925_b200 import bulk
+
+    c = BULK[k]
+    u64 = lambda xs: np.asarray(xs, dtype=np.uint64)  # noqa: E731
+    u32 = lambda xs: np.asarray(xs, dtype=np.uint32)  # noqa: E731
+    op = c["call"]
+    if op in ("prefix_words", "first_words"):
+        ctrs = c["ctrs"] if isinstance(c["ctrs"], int) else u32(c["ctrs"])
+        if op == "prefix_words":
+            got = bulk.prefix_words(c["alg"], u64(c["seeds"]), ctrs, c["nwords"], device="cpu")
+        else:
+            got = bulk.first_words(c["alg"], u64(c["seeds"]), ctrs, device="cpu")
+        assert _sha32(got) == c["sha"]
+    elif op == "source_stream_words":
+        got = bulk.AlgorithmSource(c["alg"]).stream_words(c["seed"], c["ctr"], c["n"], device="cpu")
+        assert _sha32(got) == c["sha"]
+    elif op == "philox4x32":
+        v = c["in"]
+        assert _sha32(np.stack(bulk.philox4x32(*(u32(v[x]) for x in "abcdef")))) == c["sha"]
+    elif op == "threefry4x32":
+        v = c["in"]
+        assert _sha32(np.stack(bulk.threefry4x32(*(u32(v[x]) for x in "abcdefgh")))) == c["sha"]
+    elif op == "squares_keys":
+        assert h16(np.asarray(bulk.squares_keys(u64(c["seeds"])), np.uint64).tobytes()) == c["sha"]
+    elif op == "squares32":
+        assert _sha32(bulk.squares32(u64(c["ctr"]), u64(c["key"]))) == c["sha"]
+    elif op == "tyche_init":
+        assert _sha32(np.stack(bulk.tyche_init(u64(c["seeds"]), u32(c["ctrs"])))) == c["sha"]
+    elif op == "tyche_mix":
+        v = c["in"]
+        assert _sha32(np.stack(bulk.tyche_mix(*(u32(v[x]) for x in "abcd")))) == c["sha"]
+    elif op == "tyche_advance_state":
+        assert list(bulk.tyche_advance_state(tuple(c["state"]), c["steps"])) == c["res"]
+    else:
+        raise AssertionError(op)
