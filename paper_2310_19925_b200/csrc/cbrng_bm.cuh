@@ -9,7 +9,7 @@
 // FP64 instructions per pair at the accuracy the parity tests demand
 // (<= 4 ulp(max(|z|,1)) of glibc; 3 is the worst seen over 4e7 random pairs
 // in the host prototype of exactly these formulas, fewer 3-ulp cases than
-// the r1 libm-style version). About 39 FP64 instructions per pair, from 63:
+// the r1 libm-style version). About 35 FP64 instructions per pair, from 63:
 //   u1:   never formed. f64(w0,w1) = u 2^-53 with u = (w >> 11), so
 //         u1 = v 2^-53, v = 2^53 - u an integer in [1, 2^53]: one 64-bit
 //         integer subtract and one I2F (XU pipe); the 2^-53 goes into the
@@ -27,10 +27,9 @@
 //         correction with the seed's 1/(2 sqrt): 7 ops.
 //   t:    (2 pi 2^-53) * f64(u2 bits): the same rounded value as (2 pi) * u2
 //         (scaling by 2^-53 is exact on both sides), one DMUL.
-//   sincos: quadrant from the integer u2, 2-term Cody-Waite reduction by
-//         pi/2 with DFMA, fdlibm k_sin / k_cos minimax kernels on |x| <= pi/4;
-//         cos as fma(x^4, C(x^2), 1 - x^2/2) without fdlibm's extra
-//         compensation (the tolerance allows it): 18 ops.
+//   sincos: table point j = round(128 u2) from the integer u2, reduction by
+//         j pi/64, short Taylor sin/cos on |x| <= pi/128 and the angle sum with
+//         a 129-entry {sin, cos}(j pi/64) table: 14 ops.
 #pragma once
 #include <cstdint>
 
@@ -39,19 +38,11 @@
 namespace cbrng {
 
 struct BmConst {
-    double s[6];
-    double c[6];
-    double pio2_hi, pio2_lo;
     double m2ln2_hi, m2ln2_lo;  // -2 ln2 split: ln2_hi a multiple of 2^-43
     double two_pi_2m53;         // (2 pi) * 2^-53, exact scaling of the rounded 2*math.pi
 };
 
 __constant__ BmConst c_bm = {
-    {-1.66666666666666324348e-01, 8.33333333332248946124e-03, -1.98412698298579493134e-04,
-     2.75573137070700676789e-06, -2.50507602534068634195e-08, 1.58969099521155010221e-10},
-    {4.16666666666666019037e-02, -1.38888888888741095749e-03, 2.48015872894767294178e-05,
-     -2.75573143513906633035e-07, 2.08757232129817482790e-09, -1.13596475577881948265e-11},
-    1.57079632679489655800e+00, 6.12323399573676603587e-17,
     -2.0 * 0x1.62e42fefa3800p-1, -2.0 * 0x1.ef35793c7673p-45,
     6.283185307179586 * 0x1p-53,
 };
@@ -60,12 +51,22 @@ __constant__ BmConst c_bm = {
 constexpr int BM_LOGTAB_N = 256;
 __constant__ double4 c_logtab[BM_LOGTAB_N] = CBRNG_LOGTAB_INIT;
 
-// Fill kernels read the table from shared memory (divergent indices would
-// serialise constant-bank reads); a CTA stages it once.
-__device__ __forceinline__ void bm_stage_table(double4 *s_tab) {
+// {sin, cos}(j pi/64), j = 0..128 (tools/gen_logtab.py).
+constexpr int BM_SCTAB_N = 129;
+__constant__ double2 c_sctab[BM_SCTAB_N] = CBRNG_SINCOSTAB_INIT;
+
+// Both tables in shared memory: divergent indices would serialise constant-bank
+// reads. A CTA stages them once.
+struct BmTables {
+    double4 log[BM_LOGTAB_N];
+    double2 sc[BM_SCTAB_N];
+};
+
+__device__ __forceinline__ void bm_stage_table(BmTables *t) {
     const double2 *src = reinterpret_cast<const double2 *>(c_logtab);
-    double2 *dst = reinterpret_cast<double2 *>(s_tab);
+    double2 *dst = reinterpret_cast<double2 *>(t->log);
     for (uint32_t i = threadIdx.x; i < 2 * BM_LOGTAB_N; i += blockDim.x) dst[i] = src[i];
+    for (uint32_t i = threadIdx.x; i < BM_SCTAB_N; i += blockDim.x) t->sc[i] = c_sctab[i];
     __syncthreads();
 }
 
@@ -115,41 +116,36 @@ __device__ __forceinline__ double bm_sqrt(double a) {
     return fma(h0, fma(-r1, r1, a), r1);
 }
 
-// sin(t), cos(t) for t = (2 pi) u2 in [0, 2 pi), u2 = v 2^-53. The quadrant
-// q = round(4 u2) comes from the integer v (XU conversion, no FP64 ops); x =
-// t - q pi/2 is then within pi/4 of 0 up to t's rounding, where the fdlibm
-// kernels are accurate.
-__device__ __forceinline__ void sincos_2pi(double t, uint64_t v, double &sn, double &cs) {
-    const int qlo = (int)((v + (1ull << 50)) >> 51);  // 0..4
-    const double q = (double)qlo;
-    double x = fma(-q, c_bm.pio2_hi, t);
-    x = fma(-q, c_bm.pio2_lo, x);
+// sin(t), cos(t) for t = (2 pi) u2 in [0, 2 pi), u2 = v 2^-53. The table
+// point j = round(128 u2) comes from the integer v (no FP64 op); x = t - j pi/64
+// (2-term Cody-Waite, |x| <= pi/128 up to t's rounding); sin x and cos x by
+// short Taylor polynomials (truncation < 2^-60 on that range); then the angle
+// sum with the table's sin/cos of j pi/64, which are exact zeros and ones at
+// the multiples of pi/2, so results next to a zero keep their relative
+// accuracy. 14 FP64 ops (the fdlibm-kernel form with a pi/2 reduction: 18).
+__device__ __forceinline__ void sincos_2pi(double t, uint64_t v, const double2 *sct, double &sn, double &cs) {
+    const int j = (int)((v + (1ull << 45)) >> 46);  // 0..128
+    const double jd = (double)j;
+    double x = fma(-jd, CBRNG_PI64_HI, t);
+    x = fma(-jd, CBRNG_PI64_LO, x);
     const double z = x * x;
-    // fdlibm k_sin: x + x*z*(S1 + z*r)
-    const double rs = fma(z, fma(z, fma(z, fma(z, c_bm.s[5], c_bm.s[4]), c_bm.s[3]), c_bm.s[2]), c_bm.s[1]);
-    const double sx = fma(x * z, fma(z, rs, c_bm.s[0]), x);
-    // cos: 1 - z/2 + z^2 C(z)
-    const double rc =
-        fma(z, fma(z, fma(z, fma(z, fma(z, c_bm.c[5], c_bm.c[4]), c_bm.c[3]), c_bm.c[2]), c_bm.c[1]), c_bm.c[0]);
-    const double cx = fma(z * z, rc, fma(z, -0.5, 1.0));
-    // quadrant: odd q swaps sin/cos; the signs are xor-ed into the high words
-    const bool odd = qlo & 1;
-    const double a = odd ? cx : sx;  // |sin(t)| up to sign
-    const double b = odd ? sx : cx;  // |cos(t)| up to sign
-    const int ssgn = (qlo << 30) & 0x80000000;        // q & 2
-    const int csgn = ((qlo + 1) << 30) & 0x80000000;  // (q + 1) & 2
-    sn = __hiloint2double(__double2hiint(a) ^ ssgn, __double2loint(a));
-    cs = __hiloint2double(__double2hiint(b) ^ csgn, __double2loint(b));
+    const double ps = fma(z, fma(z, -1.0 / 5040, 1.0 / 120), -1.0 / 6);
+    const double s = fma(x * z, ps, x);
+    const double pc = fma(z, fma(z, -1.0 / 720, 1.0 / 24), -0.5);
+    const double c = fma(z, pc, 1.0);
+    const double2 a = sct[j];  // {sin, cos}(j pi/64)
+    sn = fma(a.x, c, a.y * s);
+    cs = fma(a.y, c, -(a.x * s));
 }
 
-// One Box-Muller pair from one 4-word block; `tab` = c_logtab staged in shared
-// memory (fill kernels) or c_logtab itself (single-thread kernels).
-__device__ __forceinline__ void box_muller_fast(uint4 w, double &z0, double &z1, const double4 *tab) {
+// One Box-Muller pair from one 4-word block; `tab` = the tables staged in shared
+// memory (bm_stage_table).
+__device__ __forceinline__ void box_muller_fast(uint4 w, double &z0, double &z1, const BmTables *tab) {
     const uint64_t u = (((uint64_t)w.y << 32) | w.x) >> 11;
     const uint64_t u2 = (((uint64_t)w.w << 32) | w.z) >> 11;
-    const double r = bm_sqrt(bm_m2log((1ull << 53) - u, tab));
+    const double r = bm_sqrt(bm_m2log((1ull << 53) - u, tab->log));
     double s, c;
-    sincos_2pi(c_bm.two_pi_2m53 * u64_to_f64_xu(u2), u2, s, c);
+    sincos_2pi(c_bm.two_pi_2m53 * u64_to_f64_xu(u2), u2, tab->sc, s, c);
     z0 = __dmul_rn(r, c);
     z1 = __dmul_rn(r, s);
 }

@@ -15,6 +15,7 @@
 // b0 + u + 1 (a resumed, mid-block generator: 2 cipher calls per unit).
 // Squares word k of unit u uses counter (word_pos + 4u + k) mod 2^32 (bulk.py:268).
 #include <cstdlib>
+#include <type_traits>
 
 #include "cbrng_internal.cuh"
 #include "cbrng_bm.cuh"
@@ -39,7 +40,7 @@ struct FillArgs {
 // CV: where the f32 map's shift / convert / scale run (u32_to_f32_cv).
 template <int OUT, int CV = 0>
 __device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0,
-                                           const double4 *bm_tab = nullptr) {
+                                           const BmTables *bm_tab = nullptr) {
     if constexpr (OUT == OUT_U32) {
         __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
     } else if constexpr (OUT == OUT_F32) {
@@ -78,8 +79,12 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
     // before the stores.
     const uint64_t n_full = a.n_units / TILE;
     // Box-Muller's log table, staged once per CTA (cbrng_bm.cuh)
-    __shared__ double4 s_bm[OUT == OUT_NORMAL ? BM_LOGTAB_N : 1];
-    if constexpr (OUT == OUT_NORMAL) bm_stage_table(s_bm);
+    __shared__ std::conditional_t<OUT == OUT_NORMAL, BmTables, char> s_bm;
+    const BmTables *bmt = nullptr;
+    if constexpr (OUT == OUT_NORMAL) {
+        bm_stage_table(&s_bm);
+        bmt = &s_bm;
+    }
     for (uint64_t t = warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
@@ -100,12 +105,12 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
         }
 #pragma unroll
         for (int j = 0; j < ILP; j++)
-            store_unit<OUT, CV>(a.out0, a.out1, base + 32 * j, w[j], a.m24, s_bm);
+            store_unit<OUT, CV>(a.out0, a.out1, base + 32 * j, w[j], a.m24, bmt);
     }
     // Remainder (< one tile) and the partial trailing unit: the last warp of the grid.
     if (warp == nwarps - 1) {
         for (uint64_t u = n_full * TILE + lane; u < a.n_units; u += 32)
-            store_unit<OUT>(a.out0, a.out1, u, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, u), 0, s_bm);
+            store_unit<OUT>(a.out0, a.out1, u, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, u), 0, bmt);
         if (a.tail && lane == 0)
             store_tail<OUT>(a.out0, a.n_units, a.tail, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, a.n_units));
     }
@@ -115,8 +120,8 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
 // one thread walks the chain. Latency-bound (~12 dependent ALU ops per word).
 template <int OUT>
 __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1, uint32_t *state_out, uint32_t z) {
-    __shared__ double4 s_bm[OUT == OUT_NORMAL ? BM_LOGTAB_N : 1];
-    if constexpr (OUT == OUT_NORMAL) bm_stage_table(s_bm);
+    __shared__ std::conditional_t<OUT == OUT_NORMAL, BmTables, char> s_bm;
+    if constexpr (OUT == OUT_NORMAL) bm_stage_table(&s_bm);
     uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
     for (uint64_t i = 0; i < n; i++) {
         if constexpr (OUT == OUT_U32) {
@@ -137,7 +142,7 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
             tyche_mix_alu(a, b, c, d, z); w.z = b;
             tyche_mix_alu(a, b, c, d, z); w.w = b;
             double z0, z1;
-            box_muller_fast(w, z0, z1, s_bm);
+            box_muller_fast(w, z0, z1, reinterpret_cast<const BmTables *>(&s_bm));
             reinterpret_cast<double *>(out0)[i] = z0;
             reinterpret_cast<double *>(out1)[i] = z1;
         }
@@ -152,12 +157,12 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
 // with scripted generators, test_distributions.py:29-40, 178-186).
 __global__ void __launch_bounds__(256) normal2_words_kernel(const uint4 *__restrict__ w, uint64_t n_pairs,
                                                             double *__restrict__ z0, double *__restrict__ z1) {
-    __shared__ double4 s_bm[BM_LOGTAB_N];
-    bm_stage_table(s_bm);
+    __shared__ BmTables s_bm;
+    bm_stage_table(&s_bm);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pairs;
          i += (uint64_t)gridDim.x * blockDim.x) {
         double a, b;
-        box_muller_fast(w[i], a, b, s_bm);
+        box_muller_fast(w[i], a, b, &s_bm);
         z0[i] = a;
         z1[i] = b;
     }
