@@ -112,3 +112,49 @@ def test_rows256_copy_out(tma):
                        timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     assert json.loads(r.stdout.strip().splitlines()[-1]) == []
+
+
+CHILD_MISC = r"""
+import sys, json, numpy as np, torch
+sys.path.insert(0, %r)
+import paper_2310_19925_b200 as cb
+from paper_2310_19925_b200 import bulk
+from oracle import oracle as orc
+bad = []
+# Brownian, fused and per-step, from an odd start (chunked step table, wrapping counter)
+for mode in ("fused", "per_step"):
+    cfg = cb.SimConfig(300, 300, init_counter=0xFFFFFFA0, mode=mode)
+    p = cb.init_particles(cfg)
+    cb.brownian.run_steps(p, cfg, start_iteration=3)
+    ref = orc.brownian_init("philox", 300, 0xFFFFFFA0)
+    orc.brownian_steps("philox", ref, 3, 300, init_ctr=0xFFFFFFA0)
+    for got, r in zip((p.x, p.y, p.vx, p.vy), ref):
+        if not np.array_equal(got.cpu().numpy(), r): bad.append(["brownian", mode]); break
+# grids: fills, Tyche rows, Box-Muller
+for alg in ("philox", "threefry", "squares"):
+    n = (1 << 20) + 9
+    if not np.array_equal(cb.uniform_f32_array(cb.make_generator(alg, 5, 1), n).cpu().numpy(),
+                          orc.words_to_f32(orc.stream_words(alg, 5, 1, n))): bad.append(["fill", alg])
+got = bulk.prefix_uniform_f32("tyche", range(1000), 0, 256).cpu().numpy().reshape(-1)
+if not np.array_equal(got, orc.words_to_f32(orc.prefix_words_arange("tyche", 0, 1000, 0, 256))): bad.append("tyche")
+z0, z1 = cb.normal2_array(cb.make_generator("philox", 42, 0), 4099)
+r0, r1 = orc.normal2("philox", 42, 0, 4099)
+for g, r in ((z0.cpu().numpy(), r0), (z1.cpu().numpy(), r1)):
+    if not np.all(np.abs(g - r) <= 4 * np.spacing(np.maximum(np.abs(r), 1.0))): bad.append("normal2")
+print(json.dumps(bad))
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"CBRNG_BROWNIAN_TAB": "0"}, {"CBRNG_BROWNIAN_PINGPONG": "0"}, {"CBRNG_BROWNIAN_PDL": "0"},
+    {"CBRNG_GRID_MULT": "0"}, {"CBRNG_GRID_MULT": "16"}, {"CBRNG_TY_GRID": "8"}, {"CBRNG_BM_MINB": "0"},
+], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_misc_knobs(env):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, "-c", CHILD_MISC % str(ROOT)], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1]) == []
