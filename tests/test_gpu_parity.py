@@ -433,6 +433,25 @@ class TestSpotChecksAtScale:
             assert np.array_equal(out[i:i + 4].cpu().numpy(), ref), i
         del out
 
+    @pytest.mark.parametrize("alg", ["philox", "squares"])
+    def test_fill_beyond_2p32_elements(self, cb, oracle, alg):
+        """One f32 fill of 2^32 + 10 values (16 GiB; 64-bit unit indexing, and for
+        Squares the 32-bit counter wrap inside the fill, bulk.py:268): spot checks
+        around 2^32 and at both ends."""
+        import torch
+
+        n = (1 << 32) + 10
+        out = cb.uniform_f32_array(cb.make_generator(alg, 7, 3), n)
+        for i in (0, 4, (1 << 32) - 8, (1 << 32) - 4, 1 << 32, (1 << 32) + 4):
+            bc = i if alg == "squares" else i // 4
+            ref = oracle.words_to_f32(oracle.stream_words(alg, 7, 3, 4, block_ctr=bc & 0xFFFFFFFF))
+            assert np.array_equal(out[i:i + 4].cpu().numpy(), ref), i
+        ref = oracle.words_to_f32(oracle.stream_words(alg, 7, 3, 2, block_ctr=((n - 2) if alg == "squares" else (n - 2) // 4) & 0xFFFFFFFF,
+                                                     lane=0 if alg == "squares" else (n - 2) % 4))
+        assert np.array_equal(out[n - 2:].cpu().numpy(), ref)
+        del out
+        torch.cuda.empty_cache()
+
     def test_cfg5_multistream_sharded_digest(self, cb, oracle):
         """100M-stream layout, shortened to 4M streams x 256: digest of the
         whole == sum of shard digests; rows spot-checked against the oracle."""
