@@ -189,16 +189,18 @@ static int env_knob(const char *name, int dflt, int lo, int hi) {
 // B200 sweeps: 4 -> 8 lifts Philox 6411 -> 6575 GB/s, Squares 4329 -> 4416,
 // Box-Muller 2526 -> 2655 (profiles/r1o_tune.md); 8 -> 16 adds 2 % for the
 // Philox word and f32 fills and costs Squares 1.5 % (r1p_tune.md) and, with the
-// XU conversion, Threefry 2 % (r1r_tune.md).
+// XU conversion, Threefry 2 % (r1r_tune.md); 12 is 1 % faster than 8 for
+// Threefry and Squares (r1t_tune.md).
 // Box-Muller stays at 8: more pairs per thread hide the long FP64 dependency
 // chains (ncu r1e at one pair: issue 64 %, "wait" the top stall), 16 spills.
-// CBRNG_FILL_ILP=8|16 overrides for tuning runs.
+// CBRNG_FILL_ILP=8|12|16 overrides for tuning runs.
 template <int ALG, int OUT>
 static int fill_ilp() {
     static int v = [] {
-        const int dflt = (ALG == PHILOX && (OUT == OUT_U32 || OUT == OUT_F32)) ? 16 : 8;
+        constexpr bool WORDS = OUT == OUT_U32 || OUT == OUT_F32;
+        const int dflt = WORDS ? (ALG == PHILOX ? 16 : 12) : 8;
         const int x = env_knob("CBRNG_FILL_ILP", dflt, 8, 16);
-        return (OUT == OUT_U32 || OUT == OUT_F32) && x == 16 ? 16 : 8;
+        return WORDS && (x == 12 || x == 16) ? x : 8;
     }();
     return v;
 }
@@ -227,6 +229,7 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
     } else {
         if constexpr (OUT == OUT_U32 || OUT == OUT_F32) {
             if (fill_ilp<ALG, OUT>() == 16) return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV>(a, st);
+            if (fill_ilp<ALG, OUT>() == 12) return launch_fill_ilp<ALG, OUT, SKIP, 12, V, CV>(a, st);
         }
         if constexpr (OUT == OUT_NORMAL && ALG == PHILOX) {
             // register cap for the FP64 Box-Muller (CBRNG_BM_MINB=0|8: CTAs/SM the

@@ -67,7 +67,7 @@ def test_threefry_variants(v):
     assert _run({"CBRNG_TF_VARIANT": str(v)}) == []
 
 
-@pytest.mark.parametrize("ilp", [8, 16])
+@pytest.mark.parametrize("ilp", [8, 12, 16])
 def test_ilp_variants(ilp):
     assert _run({"CBRNG_FILL_ILP": str(ilp)}) == []
 
