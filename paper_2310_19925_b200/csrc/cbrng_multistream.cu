@@ -161,10 +161,11 @@ template <> struct RowGen<TYCHE> {
 // VEC: rows are 16-byte aligned (nwords % 4 == 0) -> 128-bit stores. CV: the
 // f32 conversion placement (u32_to_f32_cv). Compile-time so the copy-out is
 // branch-free.
-// Occupancy: Tyche's row state is 4 registers (32-register cap, 8 CTAs/SM);
-// the counter-based row generators keep the folded stream setup live (~20
-// registers for Philox: 4 CTAs/SM, <= 64 registers, spill-free), the others 5.
-template <int ALG> constexpr int staged_min_blocks() { return ALG == TYCHE ? 8 : (ALG == PHILOX ? 4 : 5); }
+// Occupancy: Tyche's row state is 4 registers (32-register cap, 8 CTAs/SM).
+// Philox / Threefry keep the folded stream setup live and run best uncapped
+// (86 registers, 2 CTAs/SM: the 4 staged blocks' rounds interleave; Philox rows
+// +7.5 % over the 64-register cap, profiles/r1t_tune.md); Squares 5 CTAs/SM.
+template <int ALG> constexpr int staged_min_blocks() { return ALG == TYCHE ? 8 : (ALG == SQUARES ? 5 : 2); }
 
 // CH: 16-byte chunks staged per row per round: 4 (64 B of each row per store
 // instruction, 8 rows; 16 KB/CTA) or 8 (full 128 B lines, 4 rows; 32 KB/CTA).
