@@ -282,7 +282,9 @@ static bool brownian_pdl() {
 // (6 spills there).
 template <int ALG, bool HI0, bool FOLD, int MINB>
 static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
-    auto k = brownian_steps_kernel<ALG, HI0, FOLD, (MINB > 5 ? 5 : MINB)>;
+    // per-step launches (HBM-bound, one step each) run best at 4 CTAs/SM
+    auto k = mode == CBRNG_BROWNIAN_PER_STEP && MINB > 1 ? brownian_steps_kernel<ALG, HI0, FOLD, (MINB > 4 ? 4 : MINB)>
+                                                       : brownian_steps_kernel<ALG, HI0, FOLD, (MINB > 5 ? 5 : MINB)>;
     if constexpr (ALG == PHILOX && HI0) {
         static const bool tab = [] {
             const char *e = getenv("CBRNG_BROWNIAN_TAB");
