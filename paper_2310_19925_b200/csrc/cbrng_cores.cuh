@@ -517,13 +517,52 @@ __device__ __forceinline__ uint4 squares_x4(uint64_t x0, uint64_t key) {
 struct SquaresStream {
     uint64_t key;
     uint64_t base;  // (sc << 32) * key mod 2^64
+    uint64_t k2x2;  // 2 key^2 (squares_x4_inc)
+    uint64_t ebase; // ((sc << 33) + 1) key^2 + key: E for counter 0
 };
 
 inline SquaresStream squares_stream_setup(uint64_t seed, uint32_t sc) {
     SquaresStream p;
     p.key = squares_key(seed);
     p.base = ((uint64_t)sc << 32) * p.key;
+    const uint64_t k2 = p.key * p.key;
+    p.k2x2 = 2 * k2;
+    p.ebase = (((uint64_t)sc << 33) + 1) * k2 + p.key;
     return p;
+}
+
+// Round 1 of squares32 as a 64-bit value, r = x^2 + x (before its swap).
+__device__ __forceinline__ uint64_t squares_r1(uint64_t x) {
+    const uint32_t h = (uint32_t)(x >> 32), l = (uint32_t)x;
+    const uint64_t p = (uint64_t)l * l + x;
+    const uint32_t t = mul_lo_opaque(l, h);
+    return ((uint64_t)((uint32_t)(p >> 32) + t + t) << 32) | (uint32_t)p;
+}
+
+// Rounds 2-4 from round 1's r (swapped into (h, l) = (lo r, hi r)), y = x, z = x + key.
+__device__ __forceinline__ uint32_t squares_rounds_234(uint64_t r, uint64_t y, uint64_t z) {
+    uint32_t h = (uint32_t)r, l = (uint32_t)(r >> 32);
+    squares_sq_swap(h, l, z);
+    squares_sq_swap(h, l, y);
+    const uint64_t p = (uint64_t)l * l + z;
+    const uint32_t t = mul_lo_opaque(l, h);
+    return (uint32_t)(p >> 32) + t + t;
+}
+
+// Four consecutive counters with round 1 stepped by finite differences: for
+// x_k = x_0 + k key, r_k = x_k^2 + x_k satisfies r_{k+1} = r_k + E_k with
+// E_k = 2 key x_k + key^2 + key and E_{k+1} = E_k + 2 key^2 (all mod 2^64), so
+// three of the four round-1 squarings (an IMAD.WIDE + IMAD each on the
+// FMA-heavy pipe, which bounds Squares) become 64-bit adds on the ALU pipe.
+// z_k = x_k + key = x_{k+1}.
+__device__ __forceinline__ uint4 squares_x4_inc(uint64_t x0, uint64_t e0, uint64_t key, uint64_t k2x2) {
+    const uint64_t x1 = add64_opaque(x0, key), x2 = add64_opaque(x1, key), x3 = add64_opaque(x2, key);
+    const uint64_t x4 = add64_opaque(x3, key);
+    const uint64_t e1 = add64_opaque(e0, k2x2), e2 = add64_opaque(e1, k2x2);
+    const uint64_t r0 = squares_r1(x0);
+    const uint64_t r1 = add64_opaque(r0, e0), r2 = add64_opaque(r1, e1), r3 = add64_opaque(r2, e2);
+    return make_uint4(squares_rounds_234(r0, x0, x1), squares_rounds_234(r1, x1, x2), squares_rounds_234(r2, x2, x3),
+                      squares_rounds_234(r3, x3, x4));
 }
 
 __device__ __forceinline__ uint32_t squares_stream_word(const SquaresStream &p, uint32_t bc) {

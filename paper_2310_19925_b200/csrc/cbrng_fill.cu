@@ -88,7 +88,20 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
     for (uint64_t t = warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
-        if constexpr (ALG == SQUARES && V == 1) {
+        if constexpr (ALG == SQUARES && V == 2) {
+            // no counter wrap, round 1 by finite differences (squares_x4_inc):
+            // x and E for the lane's first unit, then +128 counters per j
+            const uint32_t c0 = a.bc0 + 4u * (uint32_t)base;
+            uint64_t x = (uint64_t)c0 * a.p.key + a.p.base;
+            uint64_t e = (uint64_t)c0 * a.p.k2x2 + a.p.ebase;
+            const uint64_t sx = a.p.key << 7, se = a.p.k2x2 << 7;
+#pragma unroll
+            for (int j = 0; j < ILP; j++) {
+                w[j] = squares_x4_inc(x, e, a.p.key, a.p.k2x2);
+                x = add64_opaque(x, sx);
+                e = add64_opaque(e, se);
+            }
+        } else if constexpr (ALG == SQUARES && V == 1) {
             // no counter wrap anywhere in the fill: unit u's first product
             // x = ctr * key steps by 32 units = 128 counters per j with one
             // 64-bit add (ALU) instead of a 64-bit multiply (FMA-heavy)
@@ -265,7 +278,11 @@ static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
     constexpr int C0 = cv_default<ALG>();
     if constexpr (ALG == SQUARES) {
         // counters bc0 .. bc0 + 4*(n_units+1) - 1 never wrap: drop the per-unit check
-        if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) return launch_fill_cv<ALG, OUT, SKIP, 1>(a, st);
+        if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) {
+            // V 2: round 1 by finite differences (CBRNG_SQ_INC=0 -> V 1)
+            static const bool inc = env_knob("CBRNG_SQ_INC", 1, 0, 1) == 1;
+            return inc ? launch_fill_cv<ALG, OUT, SKIP, 2>(a, st) : launch_fill_cv<ALG, OUT, SKIP, 1>(a, st);
+        }
         return launch_fill_v<ALG, OUT, SKIP, 0, C0>(a, st);
     }
     if constexpr (ALG == THREEFRY && (OUT == OUT_U32 || OUT == OUT_F32) && !SKIP) {

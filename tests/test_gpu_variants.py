@@ -67,6 +67,12 @@ def test_threefry_variants(v):
     assert _run({"CBRNG_TF_VARIANT": str(v)}) == []
 
 
+@pytest.mark.parametrize("inc", [0, 1])
+def test_squares_round1_forms(inc):
+    """Squares round 1 as one 64-bit square per word (0) or by finite differences (1)."""
+    assert _run({"CBRNG_SQ_INC": str(inc)}) == []
+
+
 @pytest.mark.parametrize("ilp", [8, 12, 16])
 def test_ilp_variants(ilp):
     assert _run({"CBRNG_FILL_ILP": str(ilp)}) == []
