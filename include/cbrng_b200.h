@@ -92,6 +92,19 @@ int cbrng_normal2_f64(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word
  * z0/z1 [dev, f64]. Same arithmetic and tolerance as cbrng_normal2_f64. */
 int cbrng_normal2_from_words(const uint32_t *words, uint64_t n_pairs, double *z0, double *z1, void *stream);
 
+/* Batched fills: job i = cbrng_words / cbrng_uniform_f32 of (algs[i], seeds[i],
+ * stream_ctrs[i] (NULL: all 0), word_pos[i], n[i]) into outs[i] [dev], in
+ * order, same results as the per-job calls. Counter-based generators only
+ * (Tyche: CBRNG_EINVAL). With CBRNG_MULTI=1 a Philox, a Threefry and a Squares
+ * job run interleaved in one kernel (measured no faster than back-to-back
+ * launches on B200, the default). No reference counterpart: the reference
+ * fills generators one call at a time (bulk.py:223-281); this is the batched
+ * form of that call. Job arrays are host memory. */
+int cbrng_words_multi(int n_jobs, const int *algs, const uint64_t *seeds, const uint32_t *stream_ctrs,
+                      const uint64_t *word_pos, const uint64_t *n, uint32_t *const *outs, void *stream);
+int cbrng_uniform_f32_multi(int n_jobs, const int *algs, const uint64_t *seeds, const uint32_t *stream_ctrs,
+                            const uint64_t *word_pos, const uint64_t *n, float *const *outs, void *stream);
+
 /* _kernels.tyche_fill (_kernels.py:22-44): state [host, 4 x u64 < 2^32] in/out.
  * SYNCHRONOUS: waits for the stream so the final state is back in `state`. */
 int cbrng_tyche_fill(uint64_t *state, uint64_t n, uint32_t *out, void *stream);

@@ -40,6 +40,8 @@ SIGNATURES = {
     "cbrng_uniform_f64": (i32, [i32, u64, u32, u64, vp, u64, vp, vp, vp]),
     "cbrng_normal2_f64": (i32, [i32, u64, u32, u64, vp, u64, vp, vp, vp, vp]),
     "cbrng_normal2_from_words": (i32, [vp, u64, vp, vp, vp]),
+    "cbrng_words_multi": (i32, [i32, vp, vp, vp, vp, vp, vp, vp]),
+    "cbrng_uniform_f32_multi": (i32, [i32, vp, vp, vp, vp, vp, vp, vp]),
     "cbrng_tyche_fill": (i32, [vp, u64, vp, vp]),
     "cbrng_prefix_words": (i32, [i32, vp, u64, vp, u32, u64, u32, vp, vp]),
     "cbrng_prefix_uniform_f32": (i32, [i32, vp, u64, vp, u32, u64, u32, vp, vp]),

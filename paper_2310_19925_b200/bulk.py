@@ -286,6 +286,64 @@ def generator_fill(g: Generator, n_elems: int, kind: str, outs=(None, None), dev
     return res[0] if n_out == 1 else tuple(res)
 
 
+_MULTI_FN = {"words": ("cbrng_words_multi", torch.uint32), "f32": ("cbrng_uniform_f32_multi", torch.float32)}
+
+
+def fill_many(gens, n, kind: str = "f32", *, outs=None, device=None):
+    """Batched Generator.words / uniform_f32_array: job i fills n[i] (or n) values
+    from gens[i]'s current position and advances gens[i], in order, exactly as the
+    per-generator calls would (bulk.py:223-281), through one C-ABI call
+    (cbrng_uniform_f32_multi / cbrng_words_multi; CBRNG_MULTI=1 runs a Philox,
+    a Threefry and a Squares job interleaved in one kernel). Tyche generators
+    (serial streams) take the per-generator path. Returns a list of results
+    like generator_fill's.
+    """
+    if kind not in _MULTI_FN:
+        raise ValueError(f"kind must be one of {sorted(_MULTI_FN)}")
+    gens = list(gens)
+    ns = [int(n)] * len(gens) if np.isscalar(n) else [int(x) for x in n]
+    if len(ns) != len(gens):
+        raise ValueError("n must be a scalar or one count per generator")
+    if any(x < 0 for x in ns):
+        raise ValueError("word count must be non-negative")
+    outs = [None] * len(gens) if outs is None else list(outs)
+    if len(outs) != len(gens):
+        raise ValueError("outs must have one entry per generator")
+    fn_name, dtype = _MULTI_FN[kind]
+    sinks = [None if g.algorithm is Algorithm.TYCHE else _dev.Sink(k, dtype, o, device)
+             for g, k, o in zip(gens, ns, outs)]
+    res: list = [None] * len(gens)
+    jobs = []  # (index, alg, seed, ctr, word_pos, n, ptr)
+    saved = {id(g): (g._cache_pos, g._block_ctr) for g in gens if g.algorithm is not Algorithm.TYCHE}
+    for i, (g, k) in enumerate(zip(gens, ns)):
+        if g.algorithm is Algorithm.TYCHE:
+            continue
+        jobs.append((i, int(g.algorithm), g.seed, g.stream_counter, g._word_pos(), k, sinks[i].dev.data_ptr()))
+        g._advance(k)
+    if jobs:
+        m = len(jobs)
+        a = np.array([j[1] for j in jobs], np.int32)
+        sd = np.array([j[2] for j in jobs], U64)
+        ct = np.array([j[3] for j in jobs], U32)
+        wp = np.array([j[4] for j in jobs], U64)
+        nn = np.array([j[5] for j in jobs], U64)
+        pp = np.array([j[6] for j in jobs], U64)
+        st = _dev.sptr(sinks[jobs[0][0]].dev)
+        rc = getattr(_lib.lib(), fn_name)(m, a.ctypes.data, sd.ctypes.data, ct.ctypes.data, wp.ctypes.data,
+                                          nn.ctypes.data, pp.ctypes.data, st)
+        if rc != 0:
+            for g in gens:
+                if id(g) in saved:
+                    g._cache_pos, g._block_ctr = saved[id(g)]
+            _lib.check(rc, fn_name)
+    for i, g in enumerate(gens):
+        if g.algorithm is Algorithm.TYCHE:
+            res[i] = generator_fill(g, ns[i], kind, (outs[i],), device)
+        else:
+            res[i] = sinks[i].finish()
+    return res
+
+
 def generator_words(g: Generator, n: int, *, out=None, device=None):
     """Implementation of Generator.words (bulk.py:223-281); advances g in place."""
     return generator_fill(g, n, "words", (out,), device)

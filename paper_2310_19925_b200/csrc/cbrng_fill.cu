@@ -68,23 +68,15 @@ __device__ __forceinline__ void store_tail(void *out0, uint64_t u, uint32_t tail
     }
 }
 
-// MB: minimum resident CTAs per SM for the register allocator (0 = unconstrained).
-template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV, int MB = 0>
-__global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+// One fill job, warp-strided: warp `warp` of `nwarps` takes tiles warp,
+// warp + nwarps, ...; the last warp also writes the remainder and the tail.
+template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV>
+__device__ __forceinline__ void fill_job(const FillArgs<ALG> &a, uint64_t warp, uint64_t nwarps, uint32_t lane,
+                                         const BmTables *bmt) {
     constexpr uint32_t TILE = 32 * ILP;
     // Full warp tiles: no bounds checks, all ILP cipher evaluations issued
     // before the stores.
     const uint64_t n_full = a.n_units / TILE;
-    // Box-Muller's log table, staged once per CTA (cbrng_bm.cuh)
-    __shared__ std::conditional_t<OUT == OUT_NORMAL, BmTables, char> s_bm;
-    const BmTables *bmt = nullptr;
-    if constexpr (OUT == OUT_NORMAL) {
-        bm_stage_table(&s_bm);
-        bmt = &s_bm;
-    }
     for (uint64_t t = warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
@@ -126,6 +118,55 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
             store_unit<OUT>(a.out0, a.out1, u, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, u), 0, bmt);
         if (a.tail && lane == 0)
             store_tail<OUT>(a.out0, a.n_units, a.tail, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, a.n_units));
+    }
+}
+
+// MB: minimum resident CTAs per SM for the register allocator (0 = unconstrained).
+template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV, int MB = 0>
+__global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    // Box-Muller's log table, staged once per CTA (cbrng_bm.cuh)
+    __shared__ std::conditional_t<OUT == OUT_NORMAL, BmTables, char> s_bm;
+    const BmTables *bmt = nullptr;
+    if constexpr (OUT == OUT_NORMAL) {
+        bm_stage_table(&s_bm);
+        bmt = &s_bm;
+    }
+    fill_job<ALG, OUT, ILP, SKIP, V, CV>(a, warp, nwarps, lane, bmt);
+}
+
+// Several counter-based fills in one launch (cbrng_words_multi /
+// cbrng_uniform_f32_multi with CBRNG_MULTI=1). The generators bind different
+// pipes (Philox: HBM and the FMA-heavy pipe; Threefry: ALU; Squares:
+// FMA-heavy), so the kernel interleaves them on every SM: warp w runs its
+// share of each job in the order starting at job w mod 3, so about a third of
+// the resident warps run each generator at any time. Each warp's total work
+// is the same share of every job, so the warps finish together. Jobs with
+// n_units == 0 and tail == 0 are absent. Only the default fast paths:
+// block-aligned Philox/Threefry (skip 0) and non-wrapping Squares (V 2).
+template <int OUT>
+struct MultiFillArgs {
+    FillArgs<PHILOX> ph;
+    FillArgs<THREEFRY> tf;
+    FillArgs<SQUARES> sq;
+};
+
+constexpr int TF_V_DEFAULT = 4;
+
+template <int OUT, int CV, int IP, int IT, int IS, int MB>
+__global__ void __launch_bounds__(256, MB) multi_fill_kernel(const __grid_constant__ MultiFillArgs<OUT> m) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t first = (uint32_t)(warp % 3);
+#pragma unroll 1
+    for (uint32_t k = 0; k < 3; k++) {
+        const uint32_t j = first + k >= 3 ? first + k - 3 : first + k;
+        if (j == 0) fill_job<PHILOX, OUT, IP, false, 0, CV>(m.ph, warp, nwarps, lane, nullptr);
+        else if (j == 1) fill_job<THREEFRY, OUT, IT, false, TF_V_DEFAULT, CV>(m.tf, warp, nwarps, lane, nullptr);
+        else fill_job<SQUARES, OUT, IS, false, 2, CV>(m.sq, warp, nwarps, lane, nullptr);
     }
 }
 
@@ -221,7 +262,6 @@ static int fill_ilp() {
 // Default code variants (B200 sweeps, profiles/r1r_tune.md): Threefry V (see
 // block_at) and the f32 conversion placement CV (see u32_to_f32_cv) per
 // generator. CBRNG_TF_VARIANT=0..8 and CBRNG_CVT=0..5 override for tuning runs.
-constexpr int TF_V_DEFAULT = 4;
 constexpr int BM_MINB_DEFAULT = 8;  // r1s sweep: 0 -> 8 = +4 % (profiles/r1s_tune.md)
 template <int ALG> constexpr int cv_default() { return 4; }  // all three fills: SHF + I2F (XU) + FMUL
 
@@ -304,10 +344,9 @@ static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
     return launch_fill_cv<ALG, OUT, SKIP, 0>(a, st);
 }
 
-template <int ALG, int OUT>
-static int launch_fill(uint64_t seed, uint32_t sc, uint64_t word_pos, uint64_t n_units, uint32_t tail, void *out0,
-                       void *out1, cudaStream_t st) {
-    if (n_units == 0 && tail == 0) return CBRNG_OK;
+template <int ALG>
+static FillArgs<ALG> make_fill_args(uint64_t seed, uint32_t sc, uint64_t word_pos, uint64_t n_units, uint32_t tail,
+                                    void *out0, void *out1) {
     FillArgs<ALG> a;
     if constexpr (ALG == PHILOX) a.p = philox_stream_setup(seed, sc);
     else if constexpr (ALG == THREEFRY) a.p = threefry_stream_setup(seed, sc);
@@ -324,6 +363,14 @@ static int launch_fill(uint64_t seed, uint32_t sc, uint64_t word_pos, uint64_t n
     a.out0 = out0;
     a.out1 = out1;
     a.m24 = 1u << 24;
+    return a;
+}
+
+template <int ALG, int OUT>
+static int launch_fill(uint64_t seed, uint32_t sc, uint64_t word_pos, uint64_t n_units, uint32_t tail, void *out0,
+                       void *out1, cudaStream_t st) {
+    if (n_units == 0 && tail == 0) return CBRNG_OK;
+    const FillArgs<ALG> a = make_fill_args<ALG>(seed, sc, word_pos, n_units, tail, out0, out1);
     if (ALG != SQUARES && a.skip) return launch_fill_k<ALG, OUT, true>(a, st);
     return launch_fill_k<ALG, OUT, false>(a, st);
 }
@@ -360,6 +407,102 @@ static int dispatch_fill(int alg, uint64_t seed, uint32_t sc, uint64_t word_pos,
     }
 }
 
+// Fused launch of up to one Philox, one Threefry and one Squares job
+// (multi_fill_kernel), opt-in with CBRNG_MULTI=1. Measured on B200 it does not
+// beat back-to-back launches (2.77 vs 2.74 ms for the three 2^30 f32 fills of
+// configs[1], profiles/r1t_tune.md): every generator already keeps both
+// integer pipes busy and the SM's issue rate binds the mix.
+template <int OUT, int IP, int IT, int IS, int MB>
+static int launch_multi_k(const MultiFillArgs<OUT> &m, cudaStream_t st) {
+    constexpr int CV = cv_default<PHILOX>();
+    auto k = multi_fill_kernel<OUT, CV, IP, IT, IS, MB>;
+    const uint64_t units = m.ph.n_units + m.tf.n_units + m.sq.n_units;
+    const uint64_t work = (units + (FILL_BLOCK * IT) - 1) / (FILL_BLOCK * IT);
+    k<<<grid_for(k, FILL_BLOCK, 0, work ? work : 1), FILL_BLOCK, 0, st>>>(m);
+    return check_launch("multi_fill_kernel");
+}
+
+// Units per thread per tile in the fused kernel: Philox 8, Threefry 4, Squares
+// 8. The standalone ILPs (16/12/12) make the three hot loops 55 KB of code that
+// run at once and thrash the instruction cache (3.35 ms vs 2.77, r1t_tune).
+template <int OUT>
+static int launch_multi(const MultiFillArgs<OUT> &m, cudaStream_t st) {
+    return launch_multi_k<OUT, 8, 4, 8, 0>(m, st);
+}
+
+struct MultiJob {
+    int alg;
+    uint64_t seed;
+    uint32_t sc;
+    uint64_t word_pos, n;
+    void *out;
+};
+
+// Jobs are taken in order; a job joins the pending fused batch when it is on
+// the fast path (block-aligned Philox/Threefry, non-wrapping Squares) and its
+// generator's slot is free, otherwise the batch is flushed first. Off-path jobs
+// launch on their own (dispatch_fill). Results equal the per-job calls.
+template <int OUT>
+static int dispatch_multi(int n_jobs, const int *algs, const uint64_t *seeds, const uint32_t *ctrs,
+                          const uint64_t *word_pos, const uint64_t *n, void *const *outs, void *stream) {
+    clear_error();
+    CBRNG_REQUIRE(n_jobs >= 0, "n_jobs < 0");
+    if (n_jobs == 0) return CBRNG_OK;
+    CBRNG_REQUIRE(algs && seeds && word_pos && n && outs, "NULL job array");
+    for (int i = 0; i < n_jobs; i++) {
+        CBRNG_CHECK_ALG(algs[i]);
+        CBRNG_REQUIRE(algs[i] != TYCHE, "job %d: tyche is serial within a stream; use the per-stream fill", i);
+        if (n[i] >= 4 && !aligned(outs[i], 16)) {
+            set_error("job %d: output pointer not 16-byte aligned", i);
+            return CBRNG_EALIGN;
+        }
+    }
+    cudaStream_t st = as_stream(stream);
+    static const bool fused = env_knob("CBRNG_MULTI", 0, 0, 1) == 1;
+    MultiFillArgs<OUT> m{};
+    int pending = 0;  // bit per generator slot
+    MultiJob single[3];
+    auto flush = [&]() -> int {
+        int rc = CBRNG_OK;
+        if (__builtin_popcount(pending) >= 2) {
+            rc = launch_multi<OUT>(m, st);
+        } else {
+            for (int g = 0; g < 3 && rc == CBRNG_OK; g++)
+                if (pending & (1 << g))
+                    rc = dispatch_fill<OUT>(g, single[g].seed, single[g].sc, single[g].word_pos, nullptr, single[g].n,
+                                            single[g].out, nullptr, nullptr, stream);
+        }
+        m = MultiFillArgs<OUT>{};
+        pending = 0;
+        return rc;
+    };
+    for (int i = 0; i < n_jobs; i++) {
+        const int g = algs[i];
+        const uint64_t seed = g == SQUARES ? (seeds[i] & 0xFFFFFFFFull) : seeds[i];  // generators.py:256-257
+        const uint32_t sc = ctrs ? ctrs[i] : 0u;
+        const uint64_t units = n[i] / 4;
+        const uint32_t tail = (uint32_t)(n[i] % 4);
+        const bool fast = fused && (units > 0) &&
+                          (g == SQUARES ? (uint64_t)(uint32_t)word_pos[i] + 4ull * (units + 1) <= (1ull << 32)
+                                        : (word_pos[i] & 3) == 0);
+        if (!fast) {
+            const int rc = dispatch_fill<OUT>(g, seed, sc, word_pos[i], nullptr, n[i], outs[i], nullptr, nullptr, stream);
+            if (rc != CBRNG_OK) return rc;
+            continue;
+        }
+        if (pending & (1 << g)) {
+            const int rc = flush();
+            if (rc != CBRNG_OK) return rc;
+        }
+        pending |= 1 << g;
+        single[g] = MultiJob{g, seed, sc, word_pos[i], n[i], outs[i]};
+        if (g == PHILOX) m.ph = make_fill_args<PHILOX>(seed, sc, word_pos[i], units, tail, outs[i], nullptr);
+        else if (g == THREEFRY) m.tf = make_fill_args<THREEFRY>(seed, sc, word_pos[i], units, tail, outs[i], nullptr);
+        else m.sq = make_fill_args<SQUARES>(seed, sc, word_pos[i], units, tail, outs[i], nullptr);
+    }
+    return flush();
+}
+
 }  // namespace cbrng
 
 using namespace cbrng;
@@ -388,6 +531,18 @@ int cbrng_normal2_f64(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word
                       uint64_t n_pairs, double *z0, double *z1, uint32_t *tyche_state_out, void *stream) {
     return dispatch_fill<OUT_NORMAL>(alg, seed, stream_ctr, word_pos, tyche_state, n_pairs, z0, z1,
                                      tyche_state_out, stream);
+}
+
+int cbrng_words_multi(int n_jobs, const int *algs, const uint64_t *seeds, const uint32_t *stream_ctrs,
+                      const uint64_t *word_pos, const uint64_t *n, uint32_t *const *outs, void *stream) {
+    return dispatch_multi<OUT_U32>(n_jobs, algs, seeds, stream_ctrs, word_pos, n,
+                                   reinterpret_cast<void *const *>(outs), stream);
+}
+
+int cbrng_uniform_f32_multi(int n_jobs, const int *algs, const uint64_t *seeds, const uint32_t *stream_ctrs,
+                            const uint64_t *word_pos, const uint64_t *n, float *const *outs, void *stream) {
+    return dispatch_multi<OUT_F32>(n_jobs, algs, seeds, stream_ctrs, word_pos, n,
+                                   reinterpret_cast<void *const *>(outs), stream);
 }
 
 int cbrng_normal2_from_words(const uint32_t *words, uint64_t n_pairs, double *z0, double *z1, void *stream) {
