@@ -131,13 +131,19 @@ template <> struct RowGen<THREEFRY> {
     __device__ __forceinline__ uint4 next4() { return threefry_stream_block<0, true>(p, b++); }
 };
 template <> struct RowGen<SQUARES> {
-    SquaresStream p;
-    uint32_t j = 0;
+    // x = ctr * key for the row's next counter, stepped by 4 key per call (one
+    // 64-bit add instead of the 64-bit multiply j * key; rows never wrap the
+    // 32-bit counter)
+    uint64_t key, x;
     __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) {
-        p.key = squares_key(seed);
-        p.base = ((uint64_t)c << 32) * p.key;
+        key = squares_key(seed);
+        x = ((uint64_t)c << 32) * key;
     }
-    __device__ __forceinline__ uint4 next4() { uint4 w = squares_stream_word4<true>(p, j); j += 4; return w; }
+    __device__ __forceinline__ uint4 next4() {
+        const uint4 w = squares_x4(x, key);
+        x = add64_opaque(x, key << 2);
+        return w;
+    }
 };
 template <> struct RowGen<TYCHE> {
     uint32_t A, B, C, D;
@@ -165,7 +171,10 @@ template <> struct RowGen<TYCHE> {
 // Philox / Threefry keep the folded stream setup live and run best uncapped
 // (86 registers, 2 CTAs/SM: the 4 staged blocks' rounds interleave; Philox rows
 // +7.5 % over the 64-register cap, profiles/r1t_tune.md); Squares 5 CTAs/SM.
-template <int ALG> constexpr int staged_min_blocks() { return ALG == TYCHE ? 8 : (ALG == SQUARES ? 5 : 2); }
+// (Squares rows with a scalar tail, !VEC: 4, which fits them without spilling)
+template <int ALG, bool VEC = true> constexpr int staged_min_blocks() {
+    return ALG == TYCHE ? 8 : (ALG == SQUARES ? (VEC ? 5 : 4) : 2);
+}
 
 // CH: 16-byte chunks staged per row per round: 4 (64 B of each row per store
 // instruction, 8 rows; 16 KB/CTA) or 8 (full 128 B lines, 4 rows; 32 KB/CTA).
@@ -173,7 +182,7 @@ template <int ALG> constexpr int staged_min_blocks() { return ALG == TYCHE ? 8 :
 // and configs[4]); a full warp's copy-out then stores through one pointer with
 // immediate row offsets and no per-row predicates.
 template <int ALG, int OUT, bool VEC, int CV, int CH = 4, int NW = 0>
-__global__ void __launch_bounds__(256, staged_min_blocks<ALG>()) staged_prefix_kernel(const __grid_constant__ PrefixArgs a) {
+__global__ void __launch_bounds__(256, staged_min_blocks<ALG, VEC>()) staged_prefix_kernel(const __grid_constant__ PrefixArgs a) {
     static_assert(CH == 4 || CH == 8, "CH");
     constexpr uint32_t RPI = 32 / CH;  // rows per copy-out instruction
     __shared__ uint4 tile[TY_WARPS][32 * CH];
