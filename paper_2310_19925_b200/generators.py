@@ -86,6 +86,11 @@ class Block(NamedTuple):
 # kernels in `bulk` on one lane. Kept for API parity; not a hot path.
 # ---------------------------------------------------------------------------
 
+def rotl32(x: int, r: int) -> int:
+    """32-bit left rotation of a Python int (generators.py:97-98; integer helper, host only)."""
+    return ((x << r) | (x >> (32 - r))) & MASK32
+
+
 def philox_block(key, ctr) -> Block:
     from . import bulk
 

@@ -108,3 +108,10 @@ def test_bench_renderers():
     assert "threefry" in table and "words/s" in table
     csv = bench_rows_csv(rows).splitlines()
     assert csv[0] == "algorithm,length,median_ns,words_per_second" and csv[1].startswith("threefry,1,1500,")
+
+
+def test_rotl32():
+    # generators.py:97-98
+    assert G.rotl32(0x80000001, 1) == 0x00000003
+    assert G.rotl32(0x12345678, 16) == 0x56781234
+    assert G.rotl32(0xDEADBEEF, 31) == ((0xDEADBEEF >> 1) | (1 << 31)) & 0xFFFFFFFF
