@@ -128,7 +128,7 @@ template <> struct RowGen<THREEFRY> {
     ThreefryStream p;
     uint32_t b = 0;
     __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) : p(threefry_stream_setup(seed, c)) {}
-    __device__ __forceinline__ uint4 next4() { return threefry_stream_block<0, true>(p, b++); }
+    __device__ __forceinline__ uint4 next4() { return threefry_stream_block<0, true, true>(p, b++); }
 };
 template <> struct RowGen<SQUARES> {
     // x = ctr * key for the row's next counter, stepped by 4 key per call (one
