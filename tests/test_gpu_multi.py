@@ -161,3 +161,33 @@ def test_errors(cb):
         cb.fill_many([cb.make_generator("philox", 1, 0)], [-1])
     with pytest.raises(ValueError):
         cb.fill_many([cb.make_generator("philox", 1, 0)], [1, 2])
+
+
+def test_random_batches_match_oracle(cb, oracle):
+    """Random batches (generators, positions, sizes, repeats) through fill_many equal
+    the oracle's streams at each job's position; the same batches through the
+    fused kernel are covered by test_fused_kernel_matches."""
+    rng = np.random.default_rng(2310)
+    algs = ("philox", "threefry", "squares", "tyche")
+    for trial in range(12):
+        gens, meta = [], []
+        for _ in range(int(rng.integers(1, 6))):
+            a = algs[int(rng.integers(0, 4))]
+            seed, sc = int(rng.integers(0, 2**63)), int(rng.integers(0, 2**32))
+            g = cb.make_generator(a, seed, sc)
+            skip = int(rng.integers(0, 9))
+            [g.next_u32() for _ in range(skip)]
+            gens.append(g)
+            meta.append((a, seed, sc, skip))
+        # repeat one generator so a job continues its predecessor
+        gens.append(gens[0])
+        meta.append(meta[0])
+        ns = [int(rng.integers(0, 20000)) for _ in gens]
+        kind = "words" if trial % 2 else "f32"
+        got = cb.fill_many(gens, ns, kind)
+        consumed = {}
+        for out, (a, seed, sc, skip), n, g in zip(got, meta, ns, gens):
+            pos = consumed.get(id(g), skip)
+            w = oracle.stream_words(a, seed, sc, pos + n)[pos:]
+            consumed[id(g)] = pos + n
+            assert np.array_equal(host(out), w if kind == "words" else oracle.words_to_f32(w)), (trial, a, pos, n)
