@@ -378,7 +378,7 @@ static int launch_staged_ch(const PrefixArgs &a, cudaStream_t st) {
             return check_launch("staged_tma_kernel");
         }
     }
-    if constexpr (CH == 4 && ALG != THREEFRY) {  // (Threefry's folded schedule spills with it)
+    if constexpr (CH == 4) {
         if (a.nwords == 256) {
             auto k = staged_prefix_kernel<ALG, OUT, true, CV, CH, 256>;
             k<<<staged_grid<ALG>(reinterpret_cast<const void *>(k), a.n_streams), 256, 0, st>>>(a);
