@@ -337,7 +337,9 @@ static bool rows_tensor_map(CUtensorMap *m, void *out, uint64_t n_streams, uint3
 // f32 conversion placement per generator (B200 sweeps, profiles/r1r_tune.md,
 // r1t_tune.md); CBRNG_CVT_MS=0..5 overrides for tuning runs. Tyche's lean
 // 256-word copy-out prefers the shift on the multiplier (IMAD.HI) and I2FP.
-template <int ALG> constexpr int ms_cv_default() { return ALG == SQUARES ? 0 : ALG == TYCHE ? 1 : 4; }
+// Re-swept after the NW=256 Threefry rows and the stepped Squares rows (r1t_tune.md):
+// Philox rows f32 CV 0 (+2.4 % over CV 4), Squares CV 4 (+0.7 % over CV 0).
+template <int ALG> constexpr int ms_cv_default() { return ALG == PHILOX ? 0 : ALG == TYCHE ? 1 : 4; }
 
 constexpr bool MS_TMA_DEFAULT = false;
 
