@@ -131,17 +131,21 @@ template <> struct RowGen<THREEFRY> {
     __device__ __forceinline__ uint4 next4() { return threefry_stream_block<0, true, true>(p, b++); }
 };
 template <> struct RowGen<SQUARES> {
-    // x = ctr * key for the row's next counter, stepped by 4 key per call (one
-    // 64-bit add instead of the 64-bit multiply j * key; rows never wrap the
-    // 32-bit counter)
-    uint64_t key, x;
+    // x = ctr * key and E = 2 key x + key^2 + key for the row's next counter,
+    // stepped by 4 counters per call (64-bit adds; rows never wrap the 32-bit
+    // counter); round 1 of the 4 words by finite differences (squares_x4_inc)
+    uint64_t key, k2x2, x, e;
     __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) {
         key = squares_key(seed);
+        const uint64_t k2 = key * key;
+        k2x2 = 2 * k2;
         x = ((uint64_t)c << 32) * key;
+        e = (((uint64_t)c << 33) + 1) * k2 + key;
     }
     __device__ __forceinline__ uint4 next4() {
-        const uint4 w = squares_x4(x, key);
+        const uint4 w = squares_x4_inc(x, e, key, k2x2);
         x = add64_opaque(x, key << 2);
+        e = add64_opaque(e, k2x2 << 2);
         return w;
     }
 };
@@ -171,9 +175,10 @@ template <> struct RowGen<TYCHE> {
 // Philox / Threefry keep the folded stream setup live and run best uncapped
 // (86 registers, 2 CTAs/SM: the 4 staged blocks' rounds interleave; Philox rows
 // +7.5 % over the 64-register cap, profiles/r1t_tune.md); Squares 5 CTAs/SM.
-// (Squares rows with a scalar tail, !VEC: 4, which fits them without spilling)
+// (Squares: 3 CTAs/SM = 80 registers, which the 8 registers of finite-difference
+// row state need without spilling; profiles/r1t_tune.md)
 template <int ALG, bool VEC = true> constexpr int staged_min_blocks() {
-    return ALG == TYCHE ? 8 : (ALG == SQUARES ? (VEC ? 5 : 4) : 2);
+    return ALG == TYCHE ? 8 : (ALG == SQUARES ? 3 : 2);
 }
 
 // CH: 16-byte chunks staged per row per round: 4 (64 B of each row per store
