@@ -42,7 +42,7 @@ TYCHE_STREAMS, TYCHE_WORDS = 1 << 22, 256
 INT_WORK_PER_WORD = {
     "philox": ("fma_heavy", 10.28, "16 IMAD.WIDE (x2.5) + 1 IMAD per 4-word block; ALU 5.6/word"),
     "threefry": ("alu", 20.10, "37 SHF.L.W + 39 LOP3 + 4 SHF.R per 4-word block; FMA-heavy 14.9 slots/word"),
-    "squares": ("fma_heavy", 12.14, "2.3 IMAD.WIDE (x2.5) + IMAD.HI (x2) + 4.3 IMAD per word (round 1 by finite differences); ALU 9.0/word"),
+    "squares": ("fma_heavy", 12.31, "2.3 IMAD.WIDE (x2.5) + IMAD.HI (x2) + 4.5 IMAD per word (round 1 by finite differences); ALU 8.3/word"),
     "tyche": ("alu", 9.76, "4 SHF.L.W + 4 LOP3 + 1 I2FP per word + staging, + the 20-mix warm-up per 256-word row"),
 }
 PIPE_LANES_PER_CLK_SM = {"alu": 63.3, "fma_heavy": 63.2}  # measured LOP3 / IMAD rates, profiles/r1s_probe_pipes.json

@@ -57,7 +57,7 @@ def main() -> None:
     # default instantiations (cbrng_fill.cu / cbrng_multistream.cu defaults)
     print("philox  ", pipes(mix(FILL, "_ZN5cbrng11fill_kernelILi0ELi1ELi16ELb0ELi0ELi4ELi0EEEvNS_8FillArgsIXT_EEE"), 64))
     print("threefry", pipes(mix(FILL, "_ZN5cbrng11fill_kernelILi1ELi1ELi12ELb0ELi4ELi4ELi0EEEvNS_8FillArgsIXT_EEE"), 48))
-    print("squares ", pipes(mix(FILL, "_ZN5cbrng11fill_kernelILi2ELi1ELi12ELb0ELi2ELi4ELi0EEEvNS_8FillArgsIXT_EEE"), 48))
+    print("squares ", pipes(mix(FILL, "_ZN5cbrng11fill_kernelILi2ELi1ELi16ELb0ELi2ELi4ELi0EEEvNS_8FillArgsIXT_EEE"), 64))
     ty = "_ZN5cbrng20staged_prefix_kernelILi3ELi1ELb1ELi1ELi4ELi256EEEvNS_10PrefixArgsE"
     # Tyche (256-word rows, CV 1): the full-warp 16-word staging loop, plus the
     # per-row warm-up (tyche_init: a 4-mix loop body run 5 times) spread over the
