@@ -245,7 +245,8 @@ static int env_knob(const char *name, int dflt, int lo, int hi) {
 // Philox word and f32 fills and costs Squares 1.5 % (r1p_tune.md) and, with the
 // XU conversion, Threefry 2 % (r1r_tune.md); 12 is 1 % faster than 8 for
 // Threefry and Squares (r1t_tune.md); after Squares' finite-difference round 1,
-// 16 edges 12 for Squares (4836 vs 4817-4820 GB/s).
+// 16 edges 12 for the Squares f32 fill (4826 vs 4807-4809 GB/s) while 12 stays
+// ahead for its u32 words (5302-5304 vs 5180-5181).
 // Box-Muller stays at 8: more pairs per thread hide the long FP64 dependency
 // chains (ncu r1e at one pair: issue 64 %, "wait" the top stall), 16 spills.
 // CBRNG_FILL_ILP=8|12|16 overrides for tuning runs.
@@ -253,7 +254,7 @@ template <int ALG, int OUT>
 static int fill_ilp() {
     static int v = [] {
         constexpr bool WORDS = OUT == OUT_U32 || OUT == OUT_F32;
-        const int dflt = WORDS ? (ALG == THREEFRY ? 12 : 16) : 8;
+        const int dflt = WORDS ? ((ALG == THREEFRY || (ALG == SQUARES && OUT == OUT_U32)) ? 12 : 16) : 8;
         const int x = env_knob("CBRNG_FILL_ILP", dflt, 8, 16);
         return WORDS && (x == 12 || x == 16) ? x : 8;
     }();
