@@ -176,9 +176,10 @@ template <> struct RowGen<TYCHE> {
 // (86 registers, 2 CTAs/SM: the 4 staged blocks' rounds interleave; Philox rows
 // +7.5 % over the 64-register cap, profiles/r1t_tune.md); Squares 5 CTAs/SM.
 // (Squares: 3 CTAs/SM = 80 registers, which the 8 registers of finite-difference
-// row state need without spilling; profiles/r1t_tune.md)
+// row state need without spilling; Threefry: 4 CTAs/SM, 64 registers, +0.5 % on
+// u32 rows over uncapped; profiles/r1t_tune.md)
 template <int ALG, bool VEC = true> constexpr int staged_min_blocks() {
-    return ALG == TYCHE ? 8 : (ALG == SQUARES ? 3 : 2);
+    return ALG == TYCHE ? 8 : (ALG == SQUARES ? 3 : (ALG == THREEFRY ? 4 : 2));
 }
 
 // CH: 16-byte chunks staged per row per round: 4 (64 B of each row per store
