@@ -115,6 +115,19 @@ __global__ void k_wide(uint64_t *out, uint32_t a) {
     if (s == 12345) out[0] = s;
 }
 
+// IMAD.WIDE without an addend: x = lo32(x) * a as a 64-bit product (mul.wide.u32),
+// chains fed through lo32 so only the multiply sits on the loop.
+__global__ void k_wide_noadd(uint64_t *out, uint32_t a) {
+    uint64_t x[CH];
+    for (int c = 0; c < CH; c++) x[c] = threadIdx.x * 7ull + c + 1;
+    for (int i = 0; i < IT; i++)
+#pragma unroll
+        for (int c = 0; c < CH; c++) asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(x[c]) : "r"((uint32_t)(x[c] >> 7)), "r"(a));
+    uint64_t s = 0;
+    for (int c = 0; c < CH; c++) s += x[c];
+    if (s == 12345) out[0] = s;
+}
+
 template <typename K, typename... A>
 static void run(const char *name, int per_iter_instr, K k, A... args) {
     int dev = 0, sms = 0, clk = 0;
@@ -153,6 +166,7 @@ int main() {
     run("DFMA + LOP3 interleaved (1:1)", 1, k_mix_alu, d, 1.0000001, 1e-9, 0x12345u, 7u);
     run("I2F.F64.U64 (+IADD 64)", 1, k_i2f64, d, 7u);
     run("IMAD.WIDE (64-bit addend, alone)", 1, k_wide, (uint64_t *)u, 0x12345u);
+    run("IMAD.WIDE (no addend, + SHF)", 2, k_wide_noadd, (uint64_t *)u, 0x12345u);
     cudaError_t e = cudaDeviceSynchronize();
     printf("# %s\n", cudaGetErrorString(e));
     return 0;
