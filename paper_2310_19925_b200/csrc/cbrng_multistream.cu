@@ -192,6 +192,11 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG, VEC>()) staged_pre
     static_assert(CH == 4 || CH == 8, "CH");
     constexpr uint32_t RPI = 32 / CH;  // rows per copy-out instruction
     __shared__ uint4 tile[TY_WARPS][32 * CH];
+    // Tyche u32 rows of NW words: a second staging buffer, so the copy-out of
+    // group g - 1 interleaves with the generation of group g (without the f32
+    // conversion between them the staging's LDS/STG bursts fill the MIO queue)
+    constexpr bool DB = ALG == TYCHE && OUT == 0 && NW != 0 && VEC && CH == 4;
+    __shared__ std::conditional_t<DB, uint4[TY_WARPS][32 * 4], uint4[1][1]> tile2;
     const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -218,17 +223,39 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG, VEC>()) staged_pre
                 // immediate offsets k * 8 * NW words from one pointer
                 using V4 = typename std::conditional<OUT == 0, uint4, float4>::type;
                 V4 *ptr = reinterpret_cast<V4 *>(a.out) + at / 4;
-                for (uint32_t g = 0; g < (uint32_t)NW / 16; g++, ptr += 4) {
+                if constexpr (DB) {
+                    uint4 *const b1 = tile2[wib];
 #pragma unroll
-                    for (int c = 0; c < CH; c++) my[lane * CH + (c ^ wx)] = gen.next4();
+                    for (int c = 0; c < 4; c++) my[lane * 4 + (c ^ wx)] = gen.next4();
                     __syncwarp();
+                    // ptr: the group being copied out (g - 1)
+                    for (uint32_t g = 1; g < (uint32_t)NW / 16; g++, ptr += 4) {
+                        uint4 *const cur = (g & 1) ? b1 : my;
+                        const uint4 *const prev = (g & 1) ? my : b1;
 #pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        const uint4 v = my[rslot + 32 * k];
-                        if constexpr (OUT == 0) __stcs(reinterpret_cast<uint4 *>(ptr) + k * 2 * NW, v);
-                        else __stcs(reinterpret_cast<float4 *>(ptr) + k * 2 * NW, u32x4_to_f32x4<CV>(v, a.m24));
+                        for (int c = 0; c < 4; c++) {
+                            cur[lane * 4 + (c ^ wx)] = gen.next4();
+                            __stcs(reinterpret_cast<uint4 *>(ptr) + c * 2 * NW, prev[rslot + 32 * c]);
+                        }
+                        __syncwarp();
                     }
+                    const uint4 *const last = ((NW / 16 - 1) & 1) ? b1 : my;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) __stcs(reinterpret_cast<uint4 *>(ptr) + k * 2 * NW, last[rslot + 32 * k]);
                     __syncwarp();
+                } else {
+                    for (uint32_t g = 0; g < (uint32_t)NW / 16; g++, ptr += 4) {
+#pragma unroll
+                        for (int c = 0; c < CH; c++) my[lane * CH + (c ^ wx)] = gen.next4();
+                        __syncwarp();
+#pragma unroll
+                        for (int k = 0; k < 4; k++) {
+                            const uint4 v = my[rslot + 32 * k];
+                            if constexpr (OUT == 0) __stcs(reinterpret_cast<uint4 *>(ptr) + k * 2 * NW, v);
+                            else __stcs(reinterpret_cast<float4 *>(ptr) + k * 2 * NW, u32x4_to_f32x4<CV>(v, a.m24));
+                        }
+                        __syncwarp();
+                    }
                 }
                 continue;
             }
