@@ -191,3 +191,28 @@ def test_random_batches_match_oracle(cb, oracle):
             w = oracle.stream_words(a, seed, sc, pos + n)[pos:]
             consumed[id(g)] = pos + n
             assert np.array_equal(host(out), w if kind == "words" else oracle.words_to_f32(w)), (trial, a, pos, n)
+
+
+@pytest.mark.parametrize("kind", ["words", "f32"])
+def test_squares_fast_path_boundary(cb, oracle, kind):
+    """The Squares fill takes the finite-difference kernel exactly when counters
+    bc0 .. bc0 + 4 (n_units + 1) - 1 stay below 2^32 (cbrng_fill.cu launch_fill_k);
+    fills that end exactly at, one unit past and well past that boundary all equal
+    the oracle's wrapping stream (bulk.py:268)."""
+    import torch
+
+    from paper_2310_19925_b200 import _lib
+
+    lib = _lib.lib()
+    fn = lib.cbrng_words if kind == "words" else lib.cbrng_uniform_f32
+    dt = torch.uint32 if kind == "words" else torch.float32
+    n = 4 * 3000 + 3
+    units = n // 4
+    for start in ((1 << 32) - 4 * (units + 1), (1 << 32) - 4 * (units + 1) + 1, (1 << 32) - 4 * units,
+                  (1 << 32) - 2 * n):
+        out = torch.empty(n, dtype=dt, device="cuda")
+        assert fn(2, 77, 9, start, None, n, out.data_ptr(), None, None) == 0
+        torch.cuda.synchronize()
+        w = oracle.stream_words("squares", 77, 9, n, block_ctr=start & 0xFFFFFFFF)
+        ref = w if kind == "words" else oracle.words_to_f32(w)
+        assert np.array_equal(out.cpu().numpy(), ref), start
