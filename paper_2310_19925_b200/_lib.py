@@ -16,6 +16,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libcbrng_b200.so"
+TUNING_LIB_PATH = LIB_DIR / "libcbrng_b200_tuning.so"  # `make -C csrc tuning`: tools/ sweeps only
 CURAND_LIB_PATH = LIB_DIR / "libcbrng_curand_baseline.so"
 HEADER = PKG.parent / "include" / "cbrng_b200.h"
 
@@ -89,6 +90,21 @@ def build(force: bool = False) -> None:
     if force:
         subprocess.run(["make", "-s", "-C", str(PKG / "csrc"), "clean"], check=True)
     subprocess.run(cmd, check=True)
+
+
+def build_tuning() -> None:
+    """Compile libcbrng_b200_tuning.so (-DCBRNG_TUNING=1: CBRNG_* environment knobs and
+    the alternative kernel variants) for tools/ sweeps and tests/test_gpu_variants.py."""
+    subprocess.run(["make", "-s", "-j8", "-C", str(PKG / "csrc"), "tuning"], check=True)
+
+
+def use_tuning_build() -> None:
+    """Bind the tuning build instead of the product library (call before the first
+    library call of the process; tools/ and tests/test_gpu_variants.py only)."""
+    global LIB_PATH, _lib
+    if _lib is not None and LIB_PATH != TUNING_LIB_PATH:
+        raise RuntimeError("the product library is already bound in this process")
+    LIB_PATH = TUNING_LIB_PATH
 
 
 def _bind(path: Path, sigs: dict):

@@ -164,6 +164,10 @@ __global__ void __launch_bounds__(256, MINB) brownian_steps_kernel(const __grid_
         // per-step mode walks the arrays in alternating directions, so each step
         // starts on the particles the previous step wrote last — still in L2
         const uint64_t i = a.reverse ? a.n - 1 - j : j;
+        // an explicit pid array may have been written by the previous kernel on
+        // the stream (load_snapshot's unpack_records): wait before reading it.
+        // Implicit pids set up the key schedule under the previous grid's tail.
+        if (a.pid) asm volatile("griddepcontrol.wait;" ::: "memory");
         const uint64_t pid = a.pid ? a.pid[i] : a.pid_base + i;
         const Particle<ALG, HI0> P(pid);
         asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -259,22 +263,17 @@ __global__ void __launch_bounds__(256) digest_u32_kernel(const uint32_t *w, uint
     }
 }
 
-// CBRNG_BROWNIAN_PINGPONG=0 keeps every per-step launch in ascending order (A/B runs).
+// Per-step launches alternate the particle order (tuning build:
+// CBRNG_BROWNIAN_PINGPONG=0 keeps every launch ascending, for A/B runs).
 static bool brownian_pingpong() {
-    static const bool v = [] {
-        const char *e = getenv("CBRNG_BROWNIAN_PINGPONG");
-        return e ? atoi(e) != 0 : true;
-    }();
+    static const bool v = tuning_knob("CBRNG_BROWNIAN_PINGPONG", 1, 0, 1) != 0;
     return v;
 }
 
-// CBRNG_BROWNIAN_PDL=0 launches the per-step grids without programmatic
-// dependent launch (A/B runs).
+// Per-step grids use programmatic dependent launch (tuning build:
+// CBRNG_BROWNIAN_PDL=0 launches them plainly, for A/B runs).
 static bool brownian_pdl() {
-    static const bool v = [] {
-        const char *e = getenv("CBRNG_BROWNIAN_PDL");
-        return e ? atoi(e) != 0 : true;
-    }();
+    static const bool v = tuning_knob("CBRNG_BROWNIAN_PDL", 1, 0, 1) != 0;
     return v;
 }
 
@@ -286,10 +285,7 @@ static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
     auto k = mode == CBRNG_BROWNIAN_PER_STEP && MINB > 1 ? brownian_steps_kernel<ALG, HI0, FOLD, (MINB > 4 ? 4 : MINB)>
                                                        : brownian_steps_kernel<ALG, HI0, FOLD, (MINB > 5 ? 5 : MINB)>;
     if constexpr (ALG == PHILOX && HI0) {
-        static const bool tab = [] {
-            const char *e = getenv("CBRNG_BROWNIAN_TAB");
-            return e ? atoi(e) != 0 : true;
-        }();
+        static const bool tab = tuning_knob("CBRNG_BROWNIAN_TAB", 1, 0, 1) != 0;
         if (mode == CBRNG_BROWNIAN_FUSED && tab) k = brownian_fused_philox_kernel<FOLD, MINB>;
     }
     // One thread per particle: the fused kernel needs every particle resident
@@ -390,6 +386,7 @@ extern "C" {
 
 int cbrng_brownian_init(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_base, uint32_t init_ctr, double *x,
                         double *y, double *vx, double *vy, void *stream) {
+    const DeviceGuard device_guard(stream);
     CBRNG_CHECK_ALG(alg);
     clear_error();
     if (n == 0) return CBRNG_OK;
@@ -409,6 +406,7 @@ int cbrng_brownian_init(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_b
 int cbrng_brownian_steps(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_base, double *x, double *y, double *vx,
                          double *vy, uint32_t init_ctr, uint64_t first_it, uint64_t nsteps, double gamma, double mass,
                          double dt, int mode, void *stream) {
+    const DeviceGuard device_guard(stream);
     CBRNG_CHECK_ALG(alg);
     clear_error();
     CBRNG_REQUIRE(first_it >= 1, "iteration must be >= 1; counter 0 is reserved for init");
@@ -432,6 +430,7 @@ int cbrng_brownian_steps(int alg, uint64_t n, const uint64_t *pid, uint64_t pid_
 
 int cbrng_brownian_stats(uint64_t n, const uint64_t *pid, uint64_t pid_base, const double *x, const double *y,
                          const double *vx, const double *vy, int64_t *acc, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     CBRNG_REQUIRE(acc, "acc is NULL");
     if (n == 0) return CBRNG_OK;
@@ -441,6 +440,7 @@ int cbrng_brownian_stats(uint64_t n, const uint64_t *pid, uint64_t pid_base, con
 }
 
 int cbrng_digest_u32(const uint32_t *words, uint64_t n, uint64_t global_offset, uint64_t *acc, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     CBRNG_REQUIRE(acc, "acc is NULL");
     if (n == 0) return CBRNG_OK;
@@ -451,6 +451,7 @@ int cbrng_digest_u32(const uint32_t *words, uint64_t n, uint64_t global_offset, 
 
 int cbrng_pack_records(uint64_t n, const uint64_t *pid, uint64_t pid_base, const double *x, const double *y,
                        const double *vx, const double *vy, uint8_t *rec, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(x && y && vx && vy && rec, "NULL particle array or record buffer");
@@ -463,6 +464,7 @@ int cbrng_pack_records(uint64_t n, const uint64_t *pid, uint64_t pid_base, const
 
 int cbrng_unpack_records(uint64_t n, const uint8_t *rec, uint64_t *pid, double *x, double *y, double *vx,
                          double *vy, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(x && y && vx && vy && rec, "NULL particle array or record buffer");
@@ -474,6 +476,7 @@ int cbrng_unpack_records(uint64_t n, const uint8_t *rec, uint64_t *pid, double *
 }
 
 int cbrng_pid_order_check(uint64_t n, const uint64_t *pid, uint32_t *bad, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     CBRNG_REQUIRE(bad, "bad is NULL");
     if (n < 2 || !pid) return CBRNG_OK;

@@ -233,12 +233,6 @@ static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
     return check_launch("fill_kernel");
 }
 
-static int env_knob(const char *name, int dflt, int lo, int hi) {
-    const char *e = getenv(name);
-    const int x = e ? atoi(e) : dflt;
-    return (x >= lo && x <= hi) ? x : dflt;
-}
-
 // Units per thread per tile (independent cipher chains in flight per thread).
 // B200 sweeps: 4 -> 8 lifts Philox 6411 -> 6575 GB/s, Squares 4329 -> 4416,
 // Box-Muller 2526 -> 2655 (profiles/r1o_tune.md); 8 -> 16 adds 2 % for the
@@ -249,50 +243,41 @@ static int env_knob(const char *name, int dflt, int lo, int hi) {
 // ahead for its u32 words (5302-5304 vs 5180-5181).
 // Box-Muller stays at 8: more pairs per thread hide the long FP64 dependency
 // chains (ncu r1e at one pair: issue 64 %, "wait" the top stall), 16 spills.
-// CBRNG_FILL_ILP=8|12|16 overrides for tuning runs.
 template <int ALG, int OUT>
-static int fill_ilp() {
-    static int v = [] {
-        constexpr bool WORDS = OUT == OUT_U32 || OUT == OUT_F32;
-        const int dflt = WORDS ? ((ALG == THREEFRY || (ALG == SQUARES && OUT == OUT_U32)) ? 12 : 16) : 8;
-        const int x = env_knob("CBRNG_FILL_ILP", dflt, 8, 16);
-        return WORDS && (x == 12 || x == 16) ? x : 8;
-    }();
-    return v;
+constexpr int fill_ilp_default() {
+    constexpr bool WORDS = OUT == OUT_U32 || OUT == OUT_F32;
+    return WORDS ? ((ALG == THREEFRY || (ALG == SQUARES && OUT == OUT_U32)) ? 12 : 16) : 8;
 }
 
 // Default code variants (B200 sweeps, profiles/r1r_tune.md): Threefry V (see
 // block_at) and the f32 conversion placement CV (see u32_to_f32_cv) per
-// generator. CBRNG_TF_VARIANT=0..8 and CBRNG_CVT=0..5 override for tuning runs.
+// generator. Tuning build: CBRNG_FILL_ILP=8|12|16, CBRNG_TF_VARIANT=0..8,
+// CBRNG_CVT=0..5, CBRNG_BM_MINB=0|8, CBRNG_SQ_INC=0|1, CBRNG_MULTI=0|1.
 constexpr int BM_MINB_DEFAULT = 8;  // r1s sweep: 0 -> 8 = +4 % (profiles/r1s_tune.md)
 template <int ALG> constexpr int cv_default() { return 4; }  // all three fills: SHF + I2F (XU) + FMUL
-
-static int tf_variant() {
-    static int v = env_knob("CBRNG_TF_VARIANT", TF_V_DEFAULT, 0, 8);
-    return v;
-}
-template <int ALG>
-static int cv_variant() {
-    static int v = env_knob("CBRNG_CVT", cv_default<ALG>(), 0, 5);
-    return v;
-}
 
 template <int ALG, int OUT, bool SKIP, int V, int CV>
 static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
     if constexpr (SKIP) {
         return launch_fill_ilp<ALG, OUT, SKIP, 2, V, CV>(a, st);  // resumed mid-block: rare, 2 blocks per unit
+    } else if constexpr (OUT == OUT_U32 || OUT == OUT_F32) {
+        constexpr int I0 = fill_ilp_default<ALG, OUT>();
+        if constexpr (TUNING) {
+            static const int ilp = tuning_knob("CBRNG_FILL_ILP", I0, 8, 16);
+            if (ilp == 16) return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV>(a, st);
+            if (ilp == 12) return launch_fill_ilp<ALG, OUT, SKIP, 12, V, CV>(a, st);
+            return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
+        }
+        return launch_fill_ilp<ALG, OUT, SKIP, I0, V, CV>(a, st);
+    } else if constexpr (OUT == OUT_NORMAL && ALG == PHILOX) {
+        // register cap for the FP64 Box-Muller (8 CTAs/SM; 5 and 6 spill and
+        // were measured no better, profiles/r1s_tune.md)
+        if constexpr (TUNING) {
+            static const int mb = tuning_knob("CBRNG_BM_MINB", BM_MINB_DEFAULT, 0, 8);
+            if (mb != 8) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
+        }
+        return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, BM_MINB_DEFAULT>(a, st);
     } else {
-        if constexpr (OUT == OUT_U32 || OUT == OUT_F32) {
-            if (fill_ilp<ALG, OUT>() == 16) return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV>(a, st);
-            if (fill_ilp<ALG, OUT>() == 12) return launch_fill_ilp<ALG, OUT, SKIP, 12, V, CV>(a, st);
-        }
-        if constexpr (OUT == OUT_NORMAL && ALG == PHILOX) {
-            // register cap for the FP64 Box-Muller (CBRNG_BM_MINB=0|8: CTAs/SM the
-            // allocator must fit; 0 = unconstrained; 5 and 6 spill and were
-            // measured no better, profiles/r1s_tune.md)
-            static const int mb = env_knob("CBRNG_BM_MINB", BM_MINB_DEFAULT, 0, 8);
-            if (mb == 8) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, 8>(a, st);
-        }
         return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
     }
 }
@@ -302,8 +287,9 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
 template <int ALG, int OUT, bool SKIP, int V0>
 static int launch_fill_cv(const FillArgs<ALG> &a, cudaStream_t st) {
     constexpr int C0 = cv_default<ALG>();
-    if constexpr (OUT == OUT_F32 && !SKIP) {
-        switch (cv_variant<ALG>()) {
+    if constexpr (TUNING && OUT == OUT_F32 && !SKIP) {
+        static const int cv = tuning_knob("CBRNG_CVT", C0, 0, 5);
+        switch (cv) {
             case 0: return launch_fill_v<ALG, OUT, SKIP, V0, 0>(a, st);
             case 1: return launch_fill_v<ALG, OUT, SKIP, V0, 1>(a, st);
             case 2: return launch_fill_v<ALG, OUT, SKIP, V0, 2>(a, st);
@@ -321,29 +307,33 @@ static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
     if constexpr (ALG == SQUARES) {
         // counters bc0 .. bc0 + 4*(n_units+1) - 1 never wrap: drop the per-unit check
         if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) {
-            // V 2: round 1 by finite differences (CBRNG_SQ_INC=0 -> V 1)
-            static const bool inc = env_knob("CBRNG_SQ_INC", 1, 0, 1) == 1;
-            return inc ? launch_fill_cv<ALG, OUT, SKIP, 2>(a, st) : launch_fill_cv<ALG, OUT, SKIP, 1>(a, st);
+            // V 2: round 1 by finite differences (tuning: CBRNG_SQ_INC=0 -> V 1)
+            if constexpr (TUNING) {
+                static const bool inc = tuning_knob("CBRNG_SQ_INC", 1, 0, 1) == 1;
+                if (!inc) return launch_fill_cv<ALG, OUT, SKIP, 1>(a, st);
+            }
+            return launch_fill_cv<ALG, OUT, SKIP, 2>(a, st);
         }
-        return launch_fill_v<ALG, OUT, SKIP, 0, C0>(a, st);
-    }
-    if constexpr (ALG == THREEFRY && (OUT == OUT_U32 || OUT == OUT_F32) && !SKIP) {
-        if (tf_variant() != TF_V_DEFAULT) {
-            switch (tf_variant()) {
+        return launch_fill_v<ALG, OUT, SKIP, 0, C0>(a, st);  // the fill crosses the counter wrap
+    } else if constexpr (ALG == THREEFRY) {
+        if constexpr (TUNING && (OUT == OUT_U32 || OUT == OUT_F32) && !SKIP) {
+            static const int tfv = tuning_knob("CBRNG_TF_VARIANT", TF_V_DEFAULT, 0, 8);
+            switch (tfv) {
                 case 0: return launch_fill_v<ALG, OUT, SKIP, 0, C0>(a, st);
                 case 1: return launch_fill_v<ALG, OUT, SKIP, 1, C0>(a, st);
                 case 2: return launch_fill_v<ALG, OUT, SKIP, 2, C0>(a, st);
                 case 3: return launch_fill_v<ALG, OUT, SKIP, 3, C0>(a, st);
-                case 4: return launch_fill_v<ALG, OUT, SKIP, 4, C0>(a, st);
                 case 5: return launch_fill_v<ALG, OUT, SKIP, 5, C0>(a, st);
                 case 6: return launch_fill_v<ALG, OUT, SKIP, 6, C0>(a, st);
                 case 7: return launch_fill_v<ALG, OUT, SKIP, 7, C0>(a, st);
-                default: return launch_fill_v<ALG, OUT, SKIP, 8, C0>(a, st);
+                case 8: return launch_fill_v<ALG, OUT, SKIP, 8, C0>(a, st);
+                default: break;
             }
         }
+        return launch_fill_cv<ALG, OUT, SKIP, TF_V_DEFAULT>(a, st);
+    } else {
+        return launch_fill_cv<ALG, OUT, SKIP, 0>(a, st);
     }
-    if constexpr (ALG == THREEFRY) return launch_fill_cv<ALG, OUT, SKIP, TF_V_DEFAULT>(a, st);
-    return launch_fill_cv<ALG, OUT, SKIP, 0>(a, st);
 }
 
 template <int ALG>
@@ -373,7 +363,9 @@ static int launch_fill(uint64_t seed, uint32_t sc, uint64_t word_pos, uint64_t n
                        void *out1, cudaStream_t st) {
     if (n_units == 0 && tail == 0) return CBRNG_OK;
     const FillArgs<ALG> a = make_fill_args<ALG>(seed, sc, word_pos, n_units, tail, out0, out1);
-    if (ALG != SQUARES && a.skip) return launch_fill_k<ALG, OUT, true>(a, st);
+    if constexpr (ALG != SQUARES) {
+        if (a.skip) return launch_fill_k<ALG, OUT, true>(a, st);  // resumed mid-block
+    }
     return launch_fill_k<ALG, OUT, false>(a, st);
 }
 
@@ -460,14 +452,15 @@ static int dispatch_multi(int n_jobs, const int *algs, const uint64_t *seeds, co
         }
     }
     cudaStream_t st = as_stream(stream);
-    static const bool fused = env_knob("CBRNG_MULTI", 0, 0, 1) == 1;
+    // the fused multi-generator kernel measured no faster (tuning build only)
+    static const bool fused = TUNING && tuning_knob("CBRNG_MULTI", 0, 0, 1) == 1;
     MultiFillArgs<OUT> m{};
     int pending = 0;  // bit per generator slot
     MultiJob single[3];
     auto flush = [&]() -> int {
         int rc = CBRNG_OK;
         if (__builtin_popcount(pending) >= 2) {
-            rc = launch_multi<OUT>(m, st);
+            if constexpr (TUNING) rc = launch_multi<OUT>(m, st);
         } else {
             for (int g = 0; g < 3 && rc == CBRNG_OK; g++)
                 if (pending & (1 << g))
@@ -513,41 +506,48 @@ extern "C" {
 
 int cbrng_words(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos, const uint32_t *tyche_state,
                 uint64_t n, uint32_t *out, uint32_t *tyche_state_out, void *stream) {
+    const DeviceGuard device_guard(stream);
     return dispatch_fill<OUT_U32>(alg, seed, stream_ctr, word_pos, tyche_state, n, out, nullptr, tyche_state_out,
                                   stream);
 }
 
 int cbrng_uniform_f32(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos, const uint32_t *tyche_state,
                       uint64_t n, float *out, uint32_t *tyche_state_out, void *stream) {
+    const DeviceGuard device_guard(stream);
     return dispatch_fill<OUT_F32>(alg, seed, stream_ctr, word_pos, tyche_state, n, out, nullptr, tyche_state_out,
                                   stream);
 }
 
 int cbrng_uniform_f64(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos, const uint32_t *tyche_state,
                       uint64_t n, double *out, uint32_t *tyche_state_out, void *stream) {
+    const DeviceGuard device_guard(stream);
     return dispatch_fill<OUT_F64>(alg, seed, stream_ctr, word_pos, tyche_state, n, out, nullptr, tyche_state_out,
                                   stream);
 }
 
 int cbrng_normal2_f64(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos, const uint32_t *tyche_state,
                       uint64_t n_pairs, double *z0, double *z1, uint32_t *tyche_state_out, void *stream) {
+    const DeviceGuard device_guard(stream);
     return dispatch_fill<OUT_NORMAL>(alg, seed, stream_ctr, word_pos, tyche_state, n_pairs, z0, z1,
                                      tyche_state_out, stream);
 }
 
 int cbrng_words_multi(int n_jobs, const int *algs, const uint64_t *seeds, const uint32_t *stream_ctrs,
                       const uint64_t *word_pos, const uint64_t *n, uint32_t *const *outs, void *stream) {
+    const DeviceGuard device_guard(stream);
     return dispatch_multi<OUT_U32>(n_jobs, algs, seeds, stream_ctrs, word_pos, n,
                                    reinterpret_cast<void *const *>(outs), stream);
 }
 
 int cbrng_uniform_f32_multi(int n_jobs, const int *algs, const uint64_t *seeds, const uint32_t *stream_ctrs,
                             const uint64_t *word_pos, const uint64_t *n, float *const *outs, void *stream) {
+    const DeviceGuard device_guard(stream);
     return dispatch_multi<OUT_F32>(n_jobs, algs, seeds, stream_ctrs, word_pos, n,
                                    reinterpret_cast<void *const *>(outs), stream);
 }
 
 int cbrng_normal2_from_words(const uint32_t *words, uint64_t n_pairs, double *z0, double *z1, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n_pairs == 0) return CBRNG_OK;
     CBRNG_REQUIRE(words && z0 && z1, "NULL pointer");
@@ -562,6 +562,7 @@ int cbrng_normal2_from_words(const uint32_t *words, uint64_t n_pairs, double *z0
 }
 
 int cbrng_tyche_fill(uint64_t *state, uint64_t n, uint32_t *out, void *stream) {
+    const DeviceGuard device_guard(stream);
     CBRNG_REQUIRE(state != nullptr, "state is NULL");
     uint32_t s[4] = {(uint32_t)state[0], (uint32_t)state[1], (uint32_t)state[2], (uint32_t)state[3]};
     uint32_t *dev_state = nullptr;

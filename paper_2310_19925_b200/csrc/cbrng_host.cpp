@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include "cbrng_b200.h"
+#include "cbrng_internal.cuh"
 
 namespace cbrng {
 
@@ -25,12 +26,19 @@ void set_error(const char *fmt, ...) {
 
 void clear_error() { g_err[0] = 0; }
 
+int tuning_knob(const char *name, int dflt, int lo, int hi) {
+#if CBRNG_TUNING
+    const char *e = getenv(name);
+    const int x = e ? atoi(e) : dflt;
+    return (x >= lo && x <= hi) ? x : dflt;
+#else
+    (void)name; (void)lo; (void)hi;
+    return dflt;
+#endif
+}
+
 int grid_mult() {
-    static int v = [] {
-        const char *e = getenv("CBRNG_GRID_MULT");
-        int x = e ? atoi(e) : 8;
-        return x >= 0 ? x : 8;
-    }();
+    static const int v = tuning_knob("CBRNG_GRID_MULT", 8, 0, 64);
     return v;
 }
 

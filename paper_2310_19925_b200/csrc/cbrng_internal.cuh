@@ -9,7 +9,48 @@
 #include "cbrng_b200.h"
 #include "cbrng_cores.cuh"
 
+// Tuning builds. The product library (libcbrng_b200.so) is built with
+// CBRNG_TUNING=0: every launch parameter is the compile-time default measured
+// on B200, no environment variable is read and only the
+// default kernel instantiations exist. tools/ builds libcbrng_b200_tuning.so
+// with -DCBRNG_TUNING=1, where tuning_knob() reads CBRNG_* environment knobs
+// once per process and the alternative variants are compiled in, for A/B sweeps
+// (tests/test_gpu_variants.py keeps every variant bit-exact).
+#ifndef CBRNG_TUNING
+#define CBRNG_TUNING 0
+#endif
+
 namespace cbrng {
+
+constexpr bool TUNING = CBRNG_TUNING != 0;
+
+// The value of environment knob `name` in [lo, hi] (tuning build), else dflt.
+int tuning_knob(const char *name, int dflt, int lo, int hi);
+
+// Launches go to the device that owns `stream` (the tensor's device in the
+// Python layer), not whichever device happens to be current: the guard makes
+// it current for the call and restores the caller's device afterwards.
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(void *stream) {
+        if (!stream) return;
+        int want = -1;
+        if (cudaStreamGetDevice(reinterpret_cast<cudaStream_t>(stream), &want) != cudaSuccess) {
+            cudaGetLastError();  // not a stream of this context: leave the device alone, the launch reports it
+            return;
+        }
+        if (cudaGetDevice(&prev_) == cudaSuccess && prev_ != want && cudaSetDevice(want) == cudaSuccess) switched_ = true;
+    }
+    ~DeviceGuard() {
+        if (switched_) cudaSetDevice(prev_);
+    }
+    DeviceGuard(const DeviceGuard &) = delete;
+    DeviceGuard &operator=(const DeviceGuard &) = delete;
+
+  private:
+    int prev_ = 0;
+    bool switched_ = false;
+};
 
 void set_error(const char *fmt, ...);
 void clear_error();
@@ -38,8 +79,8 @@ inline int check_cuda(cudaError_t e, const char *what) {
 // CTAs (cached per kernel x device), capped by the amount of work.
 int resident_blocks(const void *kernel, int block, size_t smem);
 
-// Grid policy for the streaming kernels: CBRNG_GRID_MULT = k >= 1 launches k x
-// the resident grid (grid-stride); 0 launches one tile per warp. Default 8: the
+// Grid policy for the streaming kernels: k x the resident grid (grid-stride),
+// k = 8 (tuning build: CBRNG_GRID_MULT = k >= 1, or 0 = one tile per warp). The
 // write-only probe (tools/probe_store.py) reaches 6.2 TB/s from a resident
 // persistent grid (ncu: warps active ~60 % of theoretical) and 7.18 TB/s from a
 // 16x grid; the fills gain 1-2 % and reach 95 % warps active at 8x

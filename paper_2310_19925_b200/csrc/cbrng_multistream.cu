@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG>())
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+[[maybe_unused]] static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void *p = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -355,7 +355,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 // [n_streams][nwords] 4-byte elements, box 32 rows x 16 words, 64-byte swizzle.
-static bool rows_tensor_map(CUtensorMap *m, void *out, uint64_t n_streams, uint32_t nwords, bool f32) {
+[[maybe_unused]] static bool rows_tensor_map(CUtensorMap *m, void *out, uint64_t n_streams, uint32_t nwords, bool f32) {
     const auto encode = tensor_map_encoder();
     if (!encode || n_streams > 0x7FFFFFFFull) return false;
     const cuuint64_t dims[2] = {nwords, n_streams};
@@ -368,7 +368,7 @@ static bool rows_tensor_map(CUtensorMap *m, void *out, uint64_t n_streams, uint3
 }
 
 // f32 conversion placement per generator (B200 sweeps, profiles/r1r_tune.md,
-// r1t_tune.md); CBRNG_CVT_MS=0..5 overrides for tuning runs. Tyche's lean
+// r1t_tune.md); tuning build: CBRNG_CVT_MS=0..5. Tyche's lean
 // 256-word copy-out prefers the shift on the multiplier (IMAD.HI) and I2FP.
 // Re-swept after the NW=256 Threefry rows and the stepped Squares rows (r1t_tune.md):
 // Philox rows f32 CV 0 (+2.4 % over CV 4), Squares CV 4 (+0.7 % over CV 0).
@@ -376,18 +376,15 @@ template <int ALG> constexpr int ms_cv_default() { return ALG == PHILOX ? 0 : AL
 
 constexpr bool MS_TMA_DEFAULT = false;
 
-// Tyche: CBRNG_TY_GRID = k -> k x resident CTAs (persistent), 0 -> one CTA per
-// 256 streams.
+// Tyche (tuning build): CBRNG_TY_GRID = k -> k x resident CTAs (persistent), 0 ->
+// one CTA per 256 streams.
 constexpr int TY_GRID_DEFAULT = 0;  // one CTA per 256 streams: robust across boxes (r1t_tune.md)
 
 template <int ALG>
 static unsigned staged_grid(const void *kernel, uint64_t n_streams) {
     const uint64_t work = (n_streams + 255) / 256;
-    if constexpr (ALG == TYCHE) {
-        static const int k = [] {
-            const char *e = getenv("CBRNG_TY_GRID");
-            return e ? atoi(e) : TY_GRID_DEFAULT;
-        }();
+    if constexpr (TUNING && ALG == TYCHE) {
+        static const int k = tuning_knob("CBRNG_TY_GRID", TY_GRID_DEFAULT, 0, 64);
         if (k > 0) {
             const uint64_t g = (uint64_t)resident_blocks(kernel, 256, 0) * k;
             return (unsigned)(g < work ? g : work);
@@ -400,12 +397,9 @@ static unsigned staged_grid(const void *kernel, uint64_t n_streams) {
 
 template <int ALG, int OUT, int CV, int CH>
 static int launch_staged_ch(const PrefixArgs &a, cudaStream_t st) {
-    if constexpr (CH == 4 && ALG != THREEFRY) {
-        // TMA copy-out (CBRNG_MS_TMA=0 keeps the LDS/STG copy-out)
-        static const bool tma = [] {
-            const char *e = getenv("CBRNG_MS_TMA");
-            return e ? atoi(e) != 0 : MS_TMA_DEFAULT;
-        }();
+    if constexpr (TUNING && CH == 4 && ALG != THREEFRY) {
+        // TMA copy-out (tuning build, CBRNG_MS_TMA=1; measured no faster than the LDS/STG copy-out)
+        static const bool tma = tuning_knob("CBRNG_MS_TMA", MS_TMA_DEFAULT, 0, 1) != 0;
         CUtensorMap m;
         if (tma && a.nwords == 256 && rows_tensor_map(&m, a.out, a.n_streams, a.nwords, OUT == 1)) {
             auto k = staged_tma_kernel<ALG, OUT, CV>;
@@ -430,16 +424,13 @@ static int launch_staged_ch(const PrefixArgs &a, cudaStream_t st) {
     return check_launch("staged_prefix_kernel");
 }
 
-// Staging width (CBRNG_TY_CH=4|8 overrides for tuning runs; Tyche only).
+// Staging width (tuning build: CBRNG_TY_CH=4|8; Tyche only).
 constexpr int TY_CH_DEFAULT = 4;
 
 template <int ALG, int OUT, int CV>
 static int launch_staged_cv(const PrefixArgs &a, cudaStream_t st) {
-    if constexpr (ALG == TYCHE && OUT == 1) {  // (the u32 variant spills at CH 8)
-        static const int ch = [] {
-            const char *e = getenv("CBRNG_TY_CH");
-            return e ? atoi(e) : TY_CH_DEFAULT;
-        }();
+    if constexpr (TUNING && ALG == TYCHE && OUT == 1) {  // (the u32 variant spills at CH 8)
+        static const int ch = tuning_knob("CBRNG_TY_CH", TY_CH_DEFAULT, 4, 8);
         if (ch == 8) return launch_staged_ch<ALG, OUT, CV, 8>(a, st);
     }
     return launch_staged_ch<ALG, OUT, CV, 4>(a, st);
@@ -449,12 +440,8 @@ static int launch_staged_cv(const PrefixArgs &a, cudaStream_t st) {
 template <int ALG, int OUT>
 static int launch_staged(const PrefixArgs &a, cudaStream_t st) {
     constexpr int C0 = ms_cv_default<ALG>();
-    if constexpr (OUT == 1) {
-        static const int cv = [] {
-            const char *e = getenv("CBRNG_CVT_MS");
-            const int x = e ? atoi(e) : C0;
-            return (x >= 0 && x <= 5) ? x : C0;
-        }();
+    if constexpr (TUNING && OUT == 1) {
+        static const int cv = tuning_knob("CBRNG_CVT_MS", C0, 0, 5);
         switch (cv) {
             case 0: return launch_staged_cv<ALG, OUT, 0>(a, st);
             case 1: return launch_staged_cv<ALG, OUT, 1>(a, st);
@@ -578,16 +565,19 @@ extern "C" {
 
 int cbrng_prefix_words(int alg, const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs, uint32_t ctr_scalar,
                        uint64_t n_streams, uint32_t nwords, uint32_t *out, void *stream) {
+    const DeviceGuard device_guard(stream);
     return dispatch_prefix<0>(alg, seeds, seed_base, ctrs, ctr_scalar, n_streams, nwords, out, stream);
 }
 
 int cbrng_prefix_uniform_f32(int alg, const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs,
                              uint32_t ctr_scalar, uint64_t n_streams, uint32_t nvalues, float *out, void *stream) {
+    const DeviceGuard device_guard(stream);
     return dispatch_prefix<1>(alg, seeds, seed_base, ctrs, ctr_scalar, n_streams, nvalues, out, stream);
 }
 
 int cbrng_philox_block_lanes(const uint64_t *seeds, const uint64_t *stream_ctrs, uint64_t block_ctr, uint64_t n,
                              uint32_t *out, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(seeds && stream_ctrs && out, "NULL pointer");
@@ -598,6 +588,7 @@ int cbrng_philox_block_lanes(const uint64_t *seeds, const uint64_t *stream_ctrs,
 }
 
 int cbrng_philox4x32(const uint32_t *ctr, const uint32_t *key, uint64_t n, uint32_t *out, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(ctr && key && out, "NULL pointer");
@@ -606,6 +597,7 @@ int cbrng_philox4x32(const uint32_t *ctr, const uint32_t *key, uint64_t n, uint3
 }
 
 int cbrng_threefry4x32(const uint32_t *ctr, const uint32_t *key, int rounds, uint64_t n, uint32_t *out, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     CBRNG_REQUIRE(rounds >= 0, "rounds must be >= 0");
     if (n == 0) return CBRNG_OK;
@@ -615,6 +607,7 @@ int cbrng_threefry4x32(const uint32_t *ctr, const uint32_t *key, int rounds, uin
 }
 
 int cbrng_squares32(const uint64_t *ctr, const uint64_t *key, uint64_t n, uint32_t *out, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(ctr && key && out, "NULL pointer");
@@ -623,6 +616,7 @@ int cbrng_squares32(const uint64_t *ctr, const uint64_t *key, uint64_t n, uint32
 }
 
 int cbrng_squares_keys(const uint64_t *seeds, uint64_t n, uint64_t *keys, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(seeds && keys, "NULL pointer");
@@ -631,6 +625,7 @@ int cbrng_squares_keys(const uint64_t *seeds, uint64_t n, uint64_t *keys, void *
 }
 
 int cbrng_tyche_mix(uint32_t *state, uint64_t n, uint32_t rounds, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n == 0 || rounds == 0) return CBRNG_OK;
     CBRNG_REQUIRE(state, "NULL pointer");
@@ -640,6 +635,7 @@ int cbrng_tyche_mix(uint32_t *state, uint64_t n, uint32_t rounds, void *stream) 
 
 int cbrng_tyche_init(const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs, uint32_t ctr_scalar, uint64_t n,
                      uint32_t *state, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     if (n == 0) return CBRNG_OK;
     CBRNG_REQUIRE(state, "NULL pointer");

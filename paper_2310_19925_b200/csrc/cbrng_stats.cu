@@ -234,6 +234,7 @@ extern "C" {
 int cbrng_stream_byte_histogram(int alg, uint64_t seed, uint32_t stream_ctr, uint64_t word_pos,
                                 const uint32_t *tyche_state, uint64_t n_words, uint64_t *counts,
                                 uint32_t *tyche_state_out, void *stream) {
+    const DeviceGuard device_guard(stream);
     CBRNG_CHECK_ALG(alg);
     clear_error();
     CBRNG_REQUIRE(counts, "counts is NULL");
@@ -256,6 +257,7 @@ int cbrng_stream_byte_histogram(int alg, uint64_t seed, uint32_t stream_ctr, uin
 
 int cbrng_prefix_byte_histogram(int alg, uint64_t seed_base, uint32_t ctr0, uint32_t n_ctrs, uint64_t n_streams,
                                 uint32_t nwords, uint64_t *counts, void *stream) {
+    const DeviceGuard device_guard(stream);
     CBRNG_CHECK_ALG(alg);
     clear_error();
     CBRNG_REQUIRE(counts, "counts is NULL");
@@ -273,6 +275,7 @@ int cbrng_prefix_byte_histogram(int alg, uint64_t seed_base, uint32_t ctr0, uint
 }
 
 int cbrng_buffer_byte_histogram(const uint8_t *data, uint64_t n, uint64_t *counts, void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     CBRNG_REQUIRE(counts, "counts is NULL");
     if (n == 0) return CBRNG_OK;
@@ -285,6 +288,7 @@ int cbrng_buffer_byte_histogram(const uint8_t *data, uint64_t n, uint64_t *count
 
 int cbrng_avalanche(int alg, const uint64_t *seeds, const uint32_t *ctrs, const uint64_t *flips, uint64_t n,
                     uint64_t *out, void *stream) {
+    const DeviceGuard device_guard(stream);
     CBRNG_CHECK_ALG(alg);
     clear_error();
     CBRNG_REQUIRE(seeds && ctrs && flips && out, "NULL pointer");
@@ -303,6 +307,7 @@ int cbrng_avalanche(int alg, const uint64_t *seeds, const uint32_t *ctrs, const 
 
 int cbrng_pearson_partials(const double *a, const double *b, uint64_t n, uint32_t n_blocks, double *partials,
                            void *stream) {
+    const DeviceGuard device_guard(stream);
     clear_error();
     CBRNG_REQUIRE(a && b && partials && n_blocks > 0, "bad arguments");
     pearson_kernel<<<n_blocks, ST_BLOCK, 0, as_stream(stream)>>>(a, b, n, partials);

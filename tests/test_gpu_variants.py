@@ -1,11 +1,15 @@
 """Every tuning variant of the fill kernels is bit-exact, not just the default.
 
-The code variants (Threefry round/injection/rotation pipe placement,
-CBRNG_TF_VARIANT; f32 conversion placement, CBRNG_CVT / CBRNG_CVT_MS; ILP,
-CBRNG_FILL_ILP) are selected by environment knobs read once per process, so
-each combination runs in a fresh child process and is compared with the CPU
-oracle (the reference's algorithm, pinned to golden vectors in test_oracle.py).
-Sizes cover full warp tiles, the remainder path and a ragged tail.
+The product library ships only the measured defaults. The alternatives
+(Threefry round/injection/rotation pipe placement, CBRNG_TF_VARIANT; f32
+conversion placement, CBRNG_CVT / CBRNG_CVT_MS; ILP, CBRNG_FILL_ILP; ...) live
+in the tuning build (`make -C paper_2310_19925_b200/csrc tuning`,
+-DCBRNG_TUNING=1), where environment knobs read once per process select them.
+Each combination runs in a fresh child process bound to the tuning build and is
+compared with the CPU oracle (the reference's algorithm, pinned to golden
+vectors in test_oracle.py). Sizes cover full warp tiles, the remainder path and
+a ragged tail. Skipped when the tuning build is absent: what ships is covered
+by test_gpu_parity.py.
 """
 
 from __future__ import annotations
@@ -19,13 +23,17 @@ from pathlib import Path
 import numpy as np
 import pytest
 
-pytestmark = pytest.mark.gpu
-
 ROOT = Path(__file__).resolve().parents[1]
+TUNING_SO = ROOT / "paper_2310_19925_b200" / "_lib" / "libcbrng_b200_tuning.so"
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not TUNING_SO.exists(), reason="tuning build absent (make -C csrc tuning)")]
+
 
 CHILD = r"""
 import sys, json, numpy as np, torch
 sys.path.insert(0, %r)
+from paper_2310_19925_b200 import _lib; _lib.use_tuning_build()
 import paper_2310_19925_b200 as cb
 from paper_2310_19925_b200 import bulk
 from oracle import oracle as orc
@@ -86,6 +94,7 @@ def test_tyche_staging_width(ch):
 CHILD_ROWS256 = r"""
 import sys, json, numpy as np, torch
 sys.path.insert(0, %r)
+from paper_2310_19925_b200 import _lib; _lib.use_tuning_build()
 from paper_2310_19925_b200 import bulk
 from oracle import oracle as orc
 bad = []
@@ -123,6 +132,7 @@ def test_rows256_copy_out(tma):
 CHILD_MISC = r"""
 import sys, json, numpy as np, torch
 sys.path.insert(0, %r)
+from paper_2310_19925_b200 import _lib; _lib.use_tuning_build()
 import paper_2310_19925_b200 as cb
 from paper_2310_19925_b200 import bulk
 from oracle import oracle as orc

@@ -5,10 +5,6 @@ SEL='edge_sizes or row_shapes or resume_mid_block or random_streams or prefix_un
 timeout 1800 compute-sanitizer --tool memcheck --error-exitcode 9 --print-limit 20 \
     python -m pytest tests/test_gpu_parity.py tests/test_gpu_battery.py -m gpu -q -p no:cacheprovider -k "$SEL" \
     > gpurun_out/sanitize_memcheck.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/sanitize_memcheck.log
-# the TMA-store copy-out of 256-word rows (opt-in variant)
-CBRNG_MS_TMA=1 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 --print-limit 20 \
-    python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -k "row_shapes or prefix_uniform" \
-    > gpurun_out/sanitize_memcheck_tma.log 2>&1; echo "memcheck tma rc=$?" >> gpurun_out/sanitize_memcheck_tma.log
 timeout 1800 compute-sanitizer --tool racecheck --error-exitcode 9 --print-limit 20 \
     python -m pytest tests/test_gpu_parity.py tests/test_gpu_battery.py -m gpu -q -p no:cacheprovider \
     -k "row_shapes or random_streams or prefix_uniform or histograms_exact or interleave or normal2_within or normal2_words_edges or chunked_steps" \

@@ -1,4 +1,5 @@
-"""Fused Brownian kernel throughput (10M particles x 1000 steps) under the current env knobs."""
+"""Fused Brownian kernel throughput (10M particles x 1000 steps) under the current env knobs
+(tuning build: `make -C paper_2310_19925_b200/csrc tuning`)."""
 import json
 import sys
 from pathlib import Path
@@ -6,7 +7,9 @@ from pathlib import Path
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from paper_2310_19925_b200 import brownian  # noqa: E402
+from paper_2310_19925_b200 import _lib, brownian  # noqa: E402
+
+_lib.use_tuning_build()
 
 res = {}
 for alg in ("philox", "threefry", "squares", "tyche"):

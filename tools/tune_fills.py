@@ -1,5 +1,8 @@
 """Time the configs[1] fills under code variants (env knobs read once per process).
 
+Runs against the tuning build (`make -C paper_2310_19925_b200/csrc tuning`); the
+product library has no knobs.
+
     python tools/tune_fills.py            # sweeps CBRNG_FILL_ILP x CBRNG_GRID_MULT x CBRNG_TF_VARIANT
     TUNE_SETS="CBRNG_CVT=1;CBRNG_CVT=3,CBRNG_CVT_MS=3" python tools/tune_fills.py   # explicit env sets
 """
@@ -16,6 +19,7 @@ CHILD = r'''
 import sys, json, torch
 sys.path.insert(0, %r)
 from paper_2310_19925_b200 import _lib
+_lib.use_tuning_build()
 L = _lib.lib(); s = int(torch.cuda.current_stream().cuda_stream)
 N = 1 << 30
 out = torch.empty(N, dtype=torch.float32, device="cuda")
