@@ -1,20 +1,32 @@
 #!/usr/bin/env python
 """Benchmark of the B200-native counter-based RNG hot path (BASELINE.json).
 
-Headline (`value`): BASELINE configs[1] — uniform float32 fill of 2^30 values
-for each of the four generators on one GPU (Philox/Threefry/Squares: one
-stream, counter-parallel; Tyche: 2^22 streams x 256, Tyche being serial within
-a stream). One step = the four fills; value = samples/s over all ranks.
-Weak scaling: rank r fills counter range [r*2^30, (r+1)*2^30) of the same
-streams (Tyche: stream range), so the global result is one long stream.
+Headline (`value`, weak scaling): BASELINE configs[1] — uniform float32 fill of
+2^30 values per GPU for each of the four generators (Philox/Threefry/Squares:
+counter-parallel single streams; Tyche: 2^22 streams x 256, Tyche being serial
+within a stream). One step = the four fills; value = samples/s over all ranks.
+Rank r fills values [r 2^30, (r+1) 2^30) of the long-stream layout (value i is
+word i mod P of stream (42, i div P), P = the stream's period: 2^34 words for
+Philox/Threefry, 2^32 for Squares), so no rank repeats another's values.
 
-Side measurements on the same line: per-generator GB/s and roofline fraction,
-the paper's Brownian walk (configs[2], 10M x 10k, fused and per-step, against
-cuRAND Philox in the paper's Fig. 2 shape), Box-Muller f64 (configs[3]) and
-multi-stream words (configs[4]), cuRAND host-API fills, the e2e number through
-the public API with host buffers, and the CPU oracle baseline.
+Side rows (strong scaling: fixed totals split over the N ranks, each with an
+order-free digest that must not depend on N):
+  configs[2]  Brownian walk, 10M particles x 10k steps (pid-range shards),
+              fused and per-step, against cuRAND Philox in the paper's shape;
+  configs[3]  Box-Muller f64, 2^34 values (2^33 pairs, long-stream layout),
+              against cuRAND's curandGenerateNormalDouble;
+  configs[4]  10^8 Philox streams x 256 words (stream-range shards), against
+              the cuRAND device API in the same shape;
+each with its binding roofline (HBM and every compute pipe, the pipe work read
+live from the loaded library's SASS, tools/sass_pipes.py) and, at N = 1, the
+reference CPU path (C port, all host threads; and the reference package itself
+from baseline/_ref when installed).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--quick]
+                    [--dist-backend nccl|gloo]
+
+`--gpus N` without a launcher starts N ranks itself (torch.distributed.run,
+127.0.0.1); under torchrun the launcher's RANK / WORLD_SIZE are used.
 """
 
 from __future__ import annotations
@@ -22,30 +34,26 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import time
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tools"))
 
 METRIC = "Gsamples/s & HBM GB/s per generator; Brownian-walk particle-steps/s vs cuRAND"
 ALGS = ["philox", "threefry", "squares", "tyche"]
 N_PER_GPU = 1 << 30            # configs[1]: 2^30 f32 values per generator per GPU
 TYCHE_STREAMS, TYCHE_WORDS = 1 << 22, 256
-# INT-pipe work per output word of each headline fill, counted in the SASS main
-# loop of the default kernel (tools/sass_pipes.py): ALU-pipe instructions
-# (LOP3/SHF/IADD3/LEA/ISETP/...) or FMA-heavy slots (IMAD 1, IMAD.HI 2,
-# IMAD.WIDE 2.5 — the measured rates, profiles/r1s_probe_pipes.json). The
-# binding pipe is the one with more work per word.
-INT_WORK_PER_WORD = {
-    "philox": ("fma_heavy", 10.28, "16 IMAD.WIDE (x2.5) + 1 IMAD per 4-word block; ALU 5.6/word"),
-    "threefry": ("alu", 20.10, "37 SHF.L.W + 39 LOP3 + 4 SHF.R per 4-word block; FMA-heavy 14.9 slots/word"),
-    "squares": ("fma_heavy", 12.31, "2.3 IMAD.WIDE (x2.5) + IMAD.HI (x2) + 4.5 IMAD per word (round 1 by finite differences); ALU 8.3/word"),
-    "tyche": ("alu", 9.76, "4 SHF.L.W + 4 LOP3 + 1 I2FP per word + staging, + the 20-mix warm-up per 256-word row"),
-}
-PIPE_LANES_PER_CLK_SM = {"alu": 63.3, "fma_heavy": 63.2}  # measured LOP3 / IMAD rates, profiles/r1s_probe_pipes.json
+BR_PARTICLES, BR_STEPS = 10_000_000, 10_000          # configs[2] (total, split over ranks)
+BM_PAIRS = 1 << 33                                   # configs[3]: 2^34 values = 2^33 pairs (total)
+BM_CHUNK = 1 << 31                                   # pairs per launch group: 2 x 16 GiB buffers
+MS_STREAMS, MS_WORDS = 100_000_000, 256              # configs[4] (total)
+GOLDEN_R2 = ROOT / "tests" / "golden" / "golden_r2.json"
 
 
 def peaks() -> dict:
@@ -54,6 +62,10 @@ def peaks() -> dict:
         d = json.loads(p.read_text())
         return {"hbm_gbs": d["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)", "sm_max_mhz": d.get("sm_max_mhz")}
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
+
+
+def golden() -> dict:
+    return json.loads(GOLDEN_R2.read_text()) if GOLDEN_R2.exists() else {}
 
 
 class ClockSampler:
@@ -127,17 +139,44 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_reference(steps: int, warmup: int, args) -> dict:
-    """The reference's CPU path on the host cores: the C oracle (a restatement of
-    the reference algorithms, oracle/cbrng_oracle.c) with all host threads, on a
-    bounded sample of configs[1] per step. Returns a measurement dict."""
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` run without a launcher: start N ranks under
+    torch.distributed.run on 127.0.0.1 and return its exit code."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def host_threads() -> int:
+    """Every host core this process may run on (torchrun sets OMP_NUM_THREADS=1 for
+    its ranks; the CPU baselines run on rank 0 alone and take all the cores)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# Reference CPU path (test-infrastructure oracle: a C restatement of the
+# reference algorithms, all host threads) — the `--impl reference` arm and the
+# cpu_baseline legs. The reference package itself (numpy/numba) is timed too
+# when baseline/_ref is installed (tools/ref_package_bench.py, a subprocess).
+# ---------------------------------------------------------------------------
+
+def cpu_reference(steps: int, warmup: int, quick: bool) -> dict:
+    """configs[1] on the host: bounded sample per step."""
     import numpy as np
 
     from oracle import oracle as orc
 
     orc.build()
+    orc.set_num_threads(host_threads())
     threads = orc.num_threads()
-    sample = 1 << 25 if not args.quick else 1 << 22  # f32 values per generator per step
+    sample = 1 << 25 if not quick else 1 << 22  # f32 values per generator per step
     ty_streams = sample // TYCHE_WORDS
     buf = np.empty(sample, np.float32)
 
@@ -160,11 +199,57 @@ def cpu_reference(steps: int, warmup: int, args) -> dict:
             "seconds": dt}
 
 
+def cpu_side_baselines(quick: bool) -> dict:
+    """configs[2]/[3]/[4] on the host (C port, all threads), bounded samples."""
+    from oracle import oracle as orc
+
+    orc.set_num_threads(host_threads())
+    threads = orc.num_threads()
+    out = {}
+    n, s = (200_000, 10) if quick else (2_000_000, 20)
+    t = time.perf_counter()
+    st = orc.brownian_init("philox", n, 0)
+    orc.brownian_steps("philox", st, 1, s)
+    dt = time.perf_counter() - t
+    out["configs[2]"] = {"value": n * s / dt, "unit": "particle-steps/s", "cores": threads, "kind": "port",
+                         "sample": f"init + {s} steps of {n} particles (oracle brownian_init/steps, OpenMP)",
+                         "seconds": round(dt, 3)}
+    p = 1 << (20 if quick else 23)
+    t = time.perf_counter()
+    orc.normal2("philox", 42, 0, p)
+    dt = time.perf_counter() - t
+    out["configs[3]"] = {"value": 2 * p / dt / 1e9, "unit": "Gvalues/s", "cores": threads, "kind": "port",
+                         "sample": f"2^{p.bit_length() - 1} Box-Muller pairs (oracle words + libm, OpenMP)",
+                         "seconds": round(dt, 3)}
+    r = 1 << (16 if quick else 20)
+    t = time.perf_counter()
+    orc.prefix_words_arange("philox", 0, r, 0, MS_WORDS)
+    dt = time.perf_counter() - t
+    out["configs[4]"] = {"value": r * MS_WORDS / dt / 1e9, "unit": "Gwords/s", "cores": threads, "kind": "port",
+                         "sample": f"2^{r.bit_length() - 1} Philox streams x 256 (oracle prefix_words, OpenMP)",
+                         "seconds": round(dt, 3)}
+    return out
+
+
+def reference_package(quick: bool) -> dict | None:
+    """The reference package itself (baseline/_ref) on bounded samples, or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "cbrng").exists():
+        return None
+    env = dict(os.environ, PYTHONPATH=str(ref), NUMBA_CACHE_DIR="/tmp/numba_cache_ref")
+    cmd = [sys.executable, str(ROOT / "tools" / "ref_package_bench.py")] + (["--quick"] if quick else [])
+    try:
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # reported, never the target
+        return {"error": str(exc)[:300]}
+
+
 def run_reference_arm(args) -> None:
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    m = cpu_reference(args.steps, args.warmup, args)
+    m = cpu_reference(args.steps, args.warmup, args.quick)
     line = {"impl": "reference", "metric": METRIC, "value": m["value"], "unit": "Gsamples/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["seconds"] / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
@@ -176,30 +261,89 @@ def run_reference_arm(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Rooflines
+# ---------------------------------------------------------------------------
+
+def roofline_of(work: dict | None, units_per_s: float, bytes_per_unit: float, pk: dict, sms: int, mhz: float) -> dict:
+    """Fractions of HBM and of every compute pipe at this rate (per GPU); the
+    binding roofline is the largest fraction."""
+    import sass_pipes
+
+    hbm = units_per_s * bytes_per_unit / 1e9
+    fr = {"hbm": round(hbm / pk["hbm_gbs"], 3)}
+    if work:
+        fr.update(sass_pipes.fractions(work, units_per_s, sms, mhz))
+    bound = max(fr, key=fr.get)
+    out = {"bound": bound, "frac": fr[bound], "fractions": fr, "hbm_gbs": round(hbm, 1)}
+    if work:
+        out["per_unit"] = {k: work[k] for k in ("unit", "alu", "fma_heavy", "fp64", "xu", "issue") if k in work}
+        out["kernel"] = work.get("kernel")
+    return out
+
+
+def headline_roofline(per_gen: dict, dom: str, pk: dict, sms: int, mhz: float, traffic) -> dict:
+    """The contract's `roofline` for the dominant kernel, reported against its
+    BINDING roofline (the largest of the HBM and pipe fractions)."""
+    import sass_pipes
+
+    r = per_gen[dom]["roofline"]
+    b = r["bound"]
+    if b == "hbm":
+        achieved, peak, unit = r["hbm_gbs"], pk["hbm_gbs"], "GB/s"
+        peak_src = pk["source"]
+    else:
+        ops = per_gen[dom]["roofline"]["per_unit"][b]
+        achieved = round(ops * per_gen[dom]["gsamples_s"] * 1e9 / 1e12, 2)
+        peak = round(sass_pipes.PIPE_RATE[b] * sms * mhz * 1e6 / 1e12, 2)
+        unit = f"T thread-ops/s ({b} pipe)"
+        peak_src = (f"{sass_pipes.PIPE_RATE[b]} thread-ops/clk/SM (profiles/r1s_probe_pipes.json) x {sms} SMs x "
+                    f"{mhz:.0f} MHz (median SM clock in the timed region)")
+    return {"bound": b, "achieved": achieved, "peak": peak, "unit": unit, "frac": r["frac"], "traffic": traffic,
+            "kernel": r.get("kernel"), "fractions": r["fractions"],
+            "hbm": {"achieved": r["hbm_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": r["fractions"]["hbm"], "peak_source": pk["source"]},
+            "per_unit": r.get("per_unit"), "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": N_PER_GPU * 4,
+            "pipe_work_source": "tools/sass_pipes.py on the loaded libcbrng_b200.so (hot-loop SASS)"}
+
+
+# ---------------------------------------------------------------------------
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--quick", action="store_true", help="skip the side measurements")
+    ap.add_argument("--quick", action="store_true", help="skip the side rows (headline + e2e only)")
     ap.add_argument("--no-side", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baselines (tests)")
+    ap.add_argument("--side-scale", type=int, default=1,
+                    help="divide the side rows' totals by this (tests of the N-invariance logic; default 1 = BASELINE)")
     ap.add_argument("--dist-backend", default="nccl",
                     help="process-group backend (gloo lets the N>1 logic run several ranks on one GPU for testing)")
     args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
     if args.impl == "reference":
         run_reference_arm(args)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2310_19925_b200 as cb
+    import sass_pipes
     from paper_2310_19925_b200 import _lib, bulk, sharding
 
     rank, world, local = dist_env()
-    local = local % torch.cuda.device_count()
+    ndev = torch.cuda.device_count()
+    if world > ndev and args.dist_backend == "nccl":
+        raise SystemExit(f"{world} ranks need {world} GPUs for NCCL ({ndev} visible); "
+                         "use --dist-backend gloo to run the N>1 logic on fewer GPUs")
+    local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -208,9 +352,12 @@ def main() -> None:
         else:
             dist.init_process_group(args.dist_backend)
     lib = _lib.lib()
+    so = str(_lib.LIB_PATH)
     stream = torch.cuda.current_stream(dev)
     sptr = int(stream.cuda_stream)
     pk = peaks()
+    gold = golden()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
 
     def barrier():
         if world > 1:
@@ -224,17 +371,24 @@ def main() -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def all_ranks_true(ok: bool) -> bool:
+        if world == 1:
+            return ok
+        t = torch.tensor([0 if ok else 1], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return int(t.item()) == 0
+
     # ---------------- headline: configs[1] ----------------
     out = torch.empty(N_PER_GPU, dtype=torch.float32, device=dev)
-    word0 = rank * N_PER_GPU  # this rank's counter range of the shared stream
+    lo_val = rank * N_PER_GPU  # this rank's values of the long-stream layout
     ty_lo = rank * TYCHE_STREAMS
 
     def fill(alg: str):
         if alg == "tyche":
-            rc = lib.cbrng_prefix_uniform_f32(3, None, ty_lo, None, 0, TYCHE_STREAMS, TYCHE_WORDS, out.data_ptr(), sptr)
+            _lib.check(lib.cbrng_prefix_uniform_f32(3, None, ty_lo, None, 0, TYCHE_STREAMS, TYCHE_WORDS,
+                                                    out.data_ptr(), sptr), alg)
         else:
-            rc = lib.cbrng_uniform_f32(ALGS.index(alg), 42, 0, word0, None, N_PER_GPU, out.data_ptr(), None, sptr)
-        _lib.check(rc, alg)
+            sharding.uniform_f32_long(alg, 42, 0, lo_val, lo_val + N_PER_GPU, out)
 
     for _ in range(args.warmup):
         for a in ALGS:
@@ -256,16 +410,37 @@ def main() -> None:
         barrier()
     elapsed = max_over_ranks(t0.elapsed_time(t1) / 1e3)
     clocks = clk.summary()
+    mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz") or 1965.0
     launches = 4 * args.steps
-    samples = 4 * N_PER_GPU * args.steps * world
-    value = samples / elapsed / 1e9
-    bytes_per_fill = N_PER_GPU * 4
+    value = 4 * N_PER_GPU * args.steps * world / elapsed / 1e9
+
+    # full-array parity of this rank's range: the position-aware digest of every
+    # value (untimed), against the digests the reference package itself produced
+    # for configs[1] (tests/golden/make_golden_r2.py; rank 0's range = the N = 1 workload)
+    ref_d = gold.get("cfg1_fullsize", {}).get("values", {})
+    parity = {}
+    for a in ALGS:
+        fill(a)
+        d = int(sharding.digest_words(out.view(torch.uint32), rank * N_PER_GPU if a != "tyche" else ty_lo * 256).item())
+        parity[a] = f"{d & 0xFFFFFFFFFFFFFFFF:016x}"
+    torch.cuda.synchronize(dev)
+
+    work = {}
+    for a in ALGS:
+        try:
+            work[a] = (sass_pipes.rows_work(so, 3, 1) if a == "tyche" else sass_pipes.fill_work(so, ALGS.index(a), 1))
+        except Exception as exc:  # no cuobjdump on this host: HBM roofline only
+            work[a] = None
+            work_err = str(exc)
     per_gen = {}
     for a in ALGS:
-        ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev[a])
-        gbs = bytes_per_fill / (ms / 1e3) / 1e9
-        per_gen[a] = {"ms": round(ms, 4), "gsamples_s": round(N_PER_GPU / (ms / 1e3) / 1e9, 2),
-                      "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / pk["hbm_gbs"], 3)}
+        ms = max_over_ranks(statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev[a]))
+        rate = N_PER_GPU / (ms / 1e3)
+        per_gen[a] = {"ms": round(ms, 4), "gsamples_s": round(rate / 1e9, 2),
+                      "roofline": roofline_of(work[a], rate, 4, pk, sms, mhz),
+                      "digest": parity[a]}
+        if rank == 0 and a in ref_d:
+            per_gen[a]["matches_reference_fullsize"] = parity[a] == ref_d[a]
     dom = max(per_gen, key=lambda a: per_gen[a]["ms"])
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
@@ -273,55 +448,27 @@ def main() -> None:
         try:
             summ = json.loads(prof.read_text())
             traffic = summ.get("traffic_bytes", {}).get(f"uniform_f32_{dom}")
-            # the INT-pipe side of the roofline, from the committed ncu capture:
-            # the busiest of issue / ALU / FMA-heavy is the kernel's compute bound
-            pats = {"philox": "fill_kernel<0, 1", "threefry": "fill_kernel<1, 1", "squares": "fill_kernel<2, 1",
-                    "tyche": "staged_prefix_kernel<3, 1"}
-            for a, pat in pats.items():
-                k = next((k for k in summ.get("kernels", []) if pat in k["kernel"]), None)
-                if k:
-                    pipes = {"issue": k.get("issue_active_pct"), "alu": k.get("alu_pct"),
-                             "fma_heavy": k.get("fmaheavy_pct")}
-                    bind = max(pipes, key=lambda p_: pipes[p_] or 0)
-                    per_gen[a]["ncu"] = {**{p_: round(v, 1) for p_, v in pipes.items() if v is not None},
-                                         "binding_pipe": bind, "source": f"profiles/{summ.get('tag')}_ncu.md"}
-        except (ValueError, AttributeError, KeyError):
+        except (ValueError, AttributeError):
             traffic = None
-    roofline = {"bound": "hbm", "achieved": per_gen[dom]["hbm_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": per_gen[dom]["hbm_frac"], "traffic": traffic, "kernel": f"fill_kernel<{dom}, f32>",
-                "algorithmic_bytes_per_launch": bytes_per_fill, "peak_source": pk["source"]}
-    if "ncu" in per_gen[dom]:
-        # the slower of the two rooflines binds: for an INT-pipe-bound generator
-        # (Threefry: ALU) report the pipe's utilisation from the committed ncu capture
-        n = per_gen[dom]["ncu"]
-        roofline["compute_roofline"] = {"pipe": n["binding_pipe"], "utilization_pct": n.get(n["binding_pipe"]),
-                                        "source": n["source"]}
-    # INT-pipe roofline per generator (live: words/s over the measured pipe rate
-    # at the measured clock) and the fraction of the slower of the HBM-write and
-    # INT-pipe rooflines (the larger of the two utilisations)
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz") or 1965.0
-    for a, (pipe, ops, how) in INT_WORK_PER_WORD.items():
-        achieved = ops * N_PER_GPU / (per_gen[a]["ms"] / 1e3)
-        peak = PIPE_LANES_PER_CLK_SM[pipe] * sms * mhz * 1e6
-        per_gen[a]["int_roofline"] = {"pipe": pipe, "ops_per_word": ops, "frac": round(achieved / peak, 3)}
-        per_gen[a]["binding_frac"] = round(max(per_gen[a]["hbm_frac"], achieved / peak), 3)
-        if a == dom:
-            roofline.setdefault("compute_roofline", {}).update({
-                "pipe": pipe, "ops_per_word": ops, "ops_source": how,
-                "achieved_gops": round(achieved / 1e9, 1), "peak_gops": round(peak / 1e9, 1),
-                "frac": round(achieved / peak, 3),
-                "peak_source": f"{PIPE_LANES_PER_CLK_SM[pipe]} thread-ops/clk/SM (profiles/r1s_probe_pipes.json) "
-                               f"x {sms} SMs x {mhz:.0f} MHz (median SM clock in the timed region)"})
+    roofline = headline_roofline(per_gen, dom, pk, sms, mhz, traffic)
 
     line = {"metric": METRIC, "value": round(value, 3), "unit": "Gsamples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps * 1e3, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": "configs[1]: uniform_f32 fill, 2^30 values x 4 generators per GPU "
-                                   "(Philox/Threefry/Squares single stream seed 42 ctr 0; Tyche 2^22 streams x 256)",
+                                   "(Philox/Threefry/Squares seed 42, long-stream layout; Tyche 2^22 streams x 256)",
                        "l2": "outputs 4 GiB per fill >> 126 MB L2 (no flush needed)",
-                       "parallelism": f"counter/stream-range shards x{world}, no collective"},
+                       "parallelism": f"value-range / stream-range shards x{world}, no collective",
+                       "shards": "rank r: values [r 2^30, (r+1) 2^30) of stream counter r div 4 (Squares) "
+                                 "or 0 (Philox/Threefry); Tyche streams [r 2^22, (r+1) 2^22)"},
             "roofline": roofline, "per_generator": per_gen, "gpu_launches": launches, "clocks": clocks}
+    if ref_d and rank == 0:
+        line["parity"] = {"fullsize_digests_match_reference": all(per_gen[a].get("matches_reference_fullsize")
+                                                                  for a in ALGS),
+                          "what": "rank 0's 4 x 2^30 outputs, position-aware digest vs the reference package's "
+                                  "own outputs (tests/golden/golden_r2.json)"}
+    if any(w is None for w in work.values()):
+        line["roofline"]["pipe_work_error"] = work_err
 
     # write-only HBM ceiling for context (cudaMemsetAsync over the same 4 GiB)
     z0, z1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -331,9 +478,8 @@ def main() -> None:
         out.zero_()
     z1.record(stream)
     z1.synchronize()
-    store_gbs = bytes_per_fill * 5 / (z0.elapsed_time(z1) / 1e3) / 1e9
-    roofline["store_only_gbs"] = round(store_gbs, 1)
-    roofline["frac_of_store_only"] = round(per_gen[dom]["hbm_gbs"] / store_gbs, 3)
+    store_gbs = N_PER_GPU * 4 * 5 / (z0.elapsed_time(z1) / 1e3) / 1e9
+    roofline["hbm"]["store_only_gbs"] = round(store_gbs, 1)
 
     # ---------------- e2e through the public API, host buffers ----------------
     del out
@@ -341,14 +487,21 @@ def main() -> None:
     e2e_steps = 2
     host_out = torch.empty(N_PER_GPU, dtype=torch.float32, pin_memory=True)
     assert TYCHE_STREAMS * TYCHE_WORDS == N_PER_GPU
-    host_ty = host_out  # one 4 GiB pinned buffer per rank (8 ranks: 32 GiB of pinned host memory, not 64)
+
+    def positioned(a: str):
+        # the rank's range as the reference API expresses a position: an 18-byte
+        # state (algorithm, seed, stream counter, block counter, cache position)
+        per = sharding.words_per_stream(a)
+        s, off = divmod(lo_val, per)
+        g = cb.make_generator(a, 42, s)
+        st = cb.Generator.from_state_bytes(g.state_bytes()[:13] + (off // g.words_per_block).to_bytes(4, "little")
+                                           + b"\0")
+        return st
 
     def e2e_step():
         for a in ALGS[:3]:
-            g = cb.make_generator(a, 42, 0)
-            g._block_ctr = (word0 // 4) & 0xFFFFFFFF if a != "squares" else word0 & 0xFFFFFFFF
-            cb.uniform_f32_array(g, N_PER_GPU, out=host_out)
-        bulk.prefix_uniform_f32("tyche", range(ty_lo, ty_lo + TYCHE_STREAMS), 0, TYCHE_WORDS, out=host_ty)
+            cb.uniform_f32_array(positioned(a), N_PER_GPU, out=host_out)
+        bulk.prefix_uniform_f32("tyche", range(ty_lo, ty_lo + TYCHE_STREAMS), 0, TYCHE_WORDS, out=host_out)
 
     e2e_step()
     barrier()
@@ -359,35 +512,55 @@ def main() -> None:
     e2e_t = max_over_ranks(time.perf_counter() - t)
     line["e2e"] = {"value": round(4 * N_PER_GPU * e2e_steps * world / e2e_t / 1e9, 3), "unit": "Gsamples/s",
                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 4 * N_PER_GPU * 4,
-                   "api": "uniform_f32_array(make_generator(a, 42, 0), 2^30, out=pinned host) x3 + "
+                   "api": "uniform_f32_array(Generator.from_state_bytes(...), 2^30, out=pinned host) x3 + "
                           "bulk.prefix_uniform_f32(tyche, ..., out=pinned host)",
-                   "note": "host-side wall clock; 64 MiB chunks with the D2H copy overlapped (bulk.generator_fill -> "
-                           "_dev.pipelined_host_fill); bound by PCIe Gen5 x16 D2H (56 GB/s measured, tools/probes/probe_d2h.py)"}
-    del host_out, host_ty
+                   "note": "host-side wall clock, max over ranks; 64 MiB chunks with the D2H copy overlapped "
+                           "(bulk.generator_fill -> _dev.pipelined_host_fill); bound by PCIe Gen5 x16 D2H "
+                           "(56 GB/s measured, tools/probes/probe_d2h.py). The fills take scalar inputs only "
+                           "(seed, counter), so there is nothing to copy host->device."}
+    del host_out
 
     if not (args.quick or args.no_side):
-        line["side"] = side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ranks, pk)
-        line["gpu_launches"] = launches
+        line["side"] = side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ranks, all_ranks_true,
+                                         pk, gold, so, sms, mhz)
 
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            line["cpu_baseline"] = cpu_reference(1, 1, args)
-            line["cpu_baseline"].pop("seconds", None)
+            cpu = cpu_reference(1, 1, args.quick)
+            cpu.pop("seconds", None)
+            line["cpu_baseline"] = cpu
+            if not (args.quick or args.no_side):
+                pkg = reference_package(args.quick)
+                if pkg is not None:
+                    line["cpu_baseline"]["reference_package"] = pkg.get("configs[1]", pkg)
+                side_cpu = cpu_side_baselines(args.quick)
+                for key, row in (("configs[2]", "brownian"), ("configs[3]", "box_muller_f64"),
+                                 ("configs[4]", "multistream_words")):
+                    cb_ = side_cpu[key]
+                    if pkg is not None and key in pkg:
+                        cb_["reference_package"] = {**pkg[key], "kind": "reference"}
+                    line["side"][row]["cpu_baseline"] = cb_
         except Exception as exc:  # the baseline is reported, never the target
-            line["cpu_baseline"] = {"value": None, "error": str(exc)}
+            line.setdefault("cpu_baseline", {"value": None, "error": str(exc)})
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ranks, pk) -> dict:
+def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ranks, all_ranks_true, pk, gold, so,
+                      sms, mhz) -> dict:
     import torch
 
+    import sass_pipes
     from paper_2310_19925_b200 import _lib, brownian, sharding
 
     side = {}
     sptr = int(stream.cuda_stream)
+    k = max(1, args.side_scale)
+    BR_PARTICLES, BR_STEPS = globals()["BR_PARTICLES"] // k, max(globals()["BR_STEPS"] // k, 2)
+    BM_PAIRS, MS_STREAMS = globals()["BM_PAIRS"] // k, globals()["MS_STREAMS"] // k
+    n1 = gold.get("gpu_n1", {}) if k == 1 else {}
 
     def timed(fn, reps=1):
         fn()
@@ -400,11 +573,21 @@ def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ran
         barrier()
         return max_over_ranks(e0.elapsed_time(e1) / 1e3 / reps)
 
-    # ---- configs[2]: Brownian walk, 10M particles x 10k steps, pid-range shards ----
-    n_part, n_steps = 10_000_000, 10_000
-    lo, hi = rank * n_part, (rank + 1) * n_part  # weak scaling: each rank owns 10M pids
-    cfg = brownian.SimConfig(n_part, n_steps)
-    p = brownian.init_particles(cfg, pid_base=lo, n=hi - lo)
+    def work_or_none(fn, *a):
+        try:
+            return fn(so, *a)
+        except Exception:
+            return None
+
+    def invariant(key: str, digest: str) -> dict:
+        ref = n1.get(key)
+        return {"digest": digest, "n1_digest": ref, "gpu_count_invariant": (digest == ref) if ref else None}
+
+    # ---- configs[2]: Brownian walk, 10M particles x 10k steps, pid-range shards (strong) ----
+    lo, hi = sharding.shard_range(BR_PARTICLES, rank, world)
+    n_loc = hi - lo
+    cfg = brownian.SimConfig(BR_PARTICLES, BR_STEPS)
+    p = brownian.init_particles(cfg, pid_base=lo, n=n_loc)
     x0 = [t.clone() for t in (p.x, p.y, p.vx, p.vy)]
 
     def reset():
@@ -412,86 +595,134 @@ def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ran
             t.copy_(s)
 
     res = {}
+    digests = {}
     for mode in ("fused", "per_step"):
         reset()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        brownian.run_steps(p, brownian.SimConfig(n_part, n_steps, mode=mode))
+        brownian.run_steps(p, brownian.SimConfig(BR_PARTICLES, BR_STEPS, mode=mode))
         e1.record(stream)
         barrier()
         t = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-        res[mode] = {"seconds": round(t, 4), "psteps_per_s": n_part * n_steps * world / t}
-    acc = brownian.stats(p)
-    sharding.allreduce_sum_(acc)
-    stats = brownian.stats_summary(acc)
+        res[mode] = {"seconds": round(t, 4), "psteps_per_s": BR_PARTICLES * BR_STEPS / t}
+        acc = brownian.stats(p)
+        sharding.allreduce_sum_(acc)
+        digests[mode] = brownian.stats_summary(acc)
+    stats = digests["fused"]
     del x0
     # cuRAND Philox, paper Fig. 2 shape (state in HBM), and a register-state variant
     cr = _lib.curand_lib()
-    state = torch.empty(n_part * cr.cbrng_curand_state_bytes(), dtype=torch.uint8, device=dev)
+    state = torch.empty(max(n_loc, 1) * cr.cbrng_curand_state_bytes(), dtype=torch.uint8, device=dev)
     for fused, name in ((0, "curand_per_step"), (1, "curand_fused")):
-        cr.cbrng_curand_brownian_init(state.data_ptr(), n_part, p.x.data_ptr(), p.y.data_ptr(), p.vx.data_ptr(),
+        cr.cbrng_curand_brownian_init(state.data_ptr(), n_loc, p.x.data_ptr(), p.y.data_ptr(), p.vx.data_ptr(),
                                       p.vy.data_ptr(), sptr)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        cr.cbrng_curand_brownian_steps(state.data_ptr(), n_part, p.x.data_ptr(), p.y.data_ptr(), p.vx.data_ptr(),
-                                       p.vy.data_ptr(), n_steps, 0.1, 1.0, 0.01, fused, sptr)
+        cr.cbrng_curand_brownian_steps(state.data_ptr(), n_loc, p.x.data_ptr(), p.y.data_ptr(), p.vx.data_ptr(),
+                                       p.vy.data_ptr(), BR_STEPS, 0.1, 1.0, 0.01, fused, sptr)
         e1.record(stream)
         barrier()
         t = max_over_ranks(e0.elapsed_time(e1) / 1e3)
-        res[name] = {"seconds": round(t, 4), "psteps_per_s": n_part * n_steps * world / t}
+        res[name] = {"seconds": round(t, 4), "psteps_per_s": BR_PARTICLES * BR_STEPS / t}
     del state, p
     torch.cuda.empty_cache()
-    per_step_bytes = 64  # x, y, vx, vy read + written per particle-step
-    bw = res["per_step"]["psteps_per_s"] / world * per_step_bytes / 1e9
+    fused_rate = res["fused"]["psteps_per_s"] / world
     side["brownian"] = {
-        "config": "configs[2]: 10M particles x 10k steps per GPU, Philox, pid = particle index, counter = step",
+        "config": f"configs[2]: {BR_PARTICLES} particles x {BR_STEPS} steps in total, pid-range shards over "
+                  f"{world} GPU(s), Philox, pid = particle index, counter = step",
+        "scaling": "strong",
         **{k: {"seconds": v["seconds"], "psteps_per_s": f"{v['psteps_per_s']:.4e}"} for k, v in res.items()},
-        "speedup_vs_curand_per_step": round(res["per_step"]["psteps_per_s"] / res["curand_per_step"]["psteps_per_s"], 3),
         "speedup_fused_vs_curand_fused": round(res["fused"]["psteps_per_s"] / res["curand_fused"]["psteps_per_s"], 3),
-        "speedup_fused_vs_curand_per_step": round(res["fused"]["psteps_per_s"] / res["curand_per_step"]["psteps_per_s"], 3),
-        "per_step_hbm_gbs": round(bw, 1), "per_step_hbm_frac": round(bw / pk["hbm_gbs"], 3),
+        "speedup_vs_curand_per_step": round(res["per_step"]["psteps_per_s"] / res["curand_per_step"]["psteps_per_s"], 3),
+        "speedup_fused_vs_curand_per_step": round(res["fused"]["psteps_per_s"] / res["curand_per_step"]["psteps_per_s"],
+                                                  3),
+        "roofline_fused": roofline_of(work_or_none(sass_pipes.brownian_fused_work), fused_rate, 0, pk, sms, mhz),
+        "roofline_per_step": roofline_of(None, res["per_step"]["psteps_per_s"] / world, 64, pk, sms, mhz),
+        "note_per_step": "64 B of HBM per particle-step (x, y, vx, vy read + written); at N >= 8 a shard's "
+                         "state (<= 80 MB) fits in the 126 MB L2, so per-step strong scaling goes superlinear",
         "stats": stats,
+        **invariant("cfg2_stats_digest", stats["digest"]),
+        "modes_agree": digests["fused"]["digest"] == digests["per_step"]["digest"],
     }
 
-    # ---- configs[3]: Box-Muller f64, 2^34 values = 2^33 pairs per GPU ----
-    pairs = (1 << 33)
-    chunk = 1 << 31  # 16 GiB per output array per chunk keeps memory bounded
+    # ---- configs[3]: Box-Muller f64, 2^34 values = 2^33 pairs in total (strong) ----
+    lo, hi = sharding.shard_range(BM_PAIRS, rank, world)
+    chunk = min(BM_CHUNK, max(hi - lo, 1))
     z0 = torch.empty(chunk, dtype=torch.float64, device=dev)
     z1 = torch.empty(chunk, dtype=torch.float64, device=dev)
-    base = rank * pairs
+    pieces = [(c, min(c + chunk, hi)) for c in range(lo, hi, chunk)]
 
     def bm():
-        for c in range(pairs // chunk):
-            sharding.normal2_long("philox", 42, 0, base + c * chunk, base + (c + 1) * chunk, z0, z1)
+        for a, b in pieces:
+            sharding.normal2_long("philox", 42, 0, a, b, z0[: b - a], z1[: b - a])
 
     t = timed(bm)
-    vals = 2 * pairs * world
-    gbs = 2 * pairs * 8 / t / 1e9
-    side["box_muller_f64"] = {"config": "configs[3]: 2^34 normals (2^33 pairs) per GPU, long-stream layout",
-                              "seconds": round(t, 4), "gvalues_s": round(vals / t / 1e9, 2),
-                              "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / pk["hbm_gbs"], 3)}
-    acc = sharding.digest_words(z0[: 1 << 20].view(torch.uint32), 0)
+    acc = torch.zeros(1, dtype=torch.int64, device=dev)
+    for a, b in pieces:  # untimed verification pass: digest of every value
+        sharding.normal2_long("philox", 42, 0, a, b, z0[: b - a], z1[: b - a])
+        sharding.digest_words(z0[: b - a].view(torch.uint32), 2 * a, acc)
+        sharding.digest_words(z1[: b - a].view(torch.uint32), 2 * BM_PAIRS + 2 * a, acc)
+    sharding.allreduce_sum_(acc)
+    bm_digest = f"{int(acc.item()) & 0xFFFFFFFFFFFFFFFF:016x}"
+    # cuRAND Philox host API, the same 2^34 doubles (curandGenerateNormalDouble), this rank's share
+    cr = _lib.curand_lib()
+    g = cr.cbrng_curand_create(42, sptr)
+    cr.cbrng_curand_set_offset(g, 4 * lo)
+
+    def cu_bm():
+        for a, b in pieces:
+            _lib.check(0 if cr.cbrng_curand_normal_f64(g, z0.data_ptr(), b - a) == 0 else -3, "curand normal")
+            _lib.check(0 if cr.cbrng_curand_normal_f64(g, z1.data_ptr(), b - a) == 0 else -3, "curand normal")
+
+    t_cu = timed(cu_bm)
+    cr.cbrng_curand_destroy(g)
+    pairs_s = BM_PAIRS / t / world
+    side["box_muller_f64"] = {
+        "config": f"configs[3]: 2^34 normals (2^33 pairs) in total, long-stream layout, pair-range shards over "
+                  f"{world} GPU(s)",
+        "scaling": "strong",
+        "seconds": round(t, 4), "gvalues_s": round(2 * BM_PAIRS / t / 1e9, 2),
+        "roofline": roofline_of(work_or_none(sass_pipes.fill_work, 0, 3), pairs_s, 16, pk, sms, mhz),
+        "curand_normal_double": {"seconds": round(t_cu, 4), "gvalues_s": round(2 * BM_PAIRS / t_cu / 1e9, 2),
+                                 "api": "curandGenerateNormalDouble, CURAND_RNG_PSEUDO_PHILOX4_32_10"},
+        "speedup_vs_curand": round(t_cu / t, 3),
+        **invariant("cfg3_digest", bm_digest),
+    }
     del z0, z1
     torch.cuda.empty_cache()
 
-    # ---- configs[4]: 100M streams x 256 words per GPU (stream-range shards) ----
-    n_str, nw = 100_000_000, 256
-    w = torch.empty(n_str * nw, dtype=torch.uint32, device=dev)
-    s_lo = rank * n_str
+    # ---- configs[4]: 1e8 streams x 256 words in total, stream-range shards (strong) ----
+    lo, hi = sharding.shard_range(MS_STREAMS, rank, world)
+    w = torch.empty(max(hi - lo, 1) * MS_WORDS, dtype=torch.uint32, device=dev)
 
     def ms():
-        _lib.check(lib.cbrng_prefix_words(0, None, s_lo, None, 0, n_str, nw, w.data_ptr(), sptr), "prefix")
+        _lib.check(lib.cbrng_prefix_words(0, None, lo, None, 0, hi - lo, MS_WORDS, w.data_ptr(), sptr), "prefix")
 
-    t = timed(ms)
-    gbs = n_str * nw * 4 / t / 1e9
-    d = sharding.digest_words(w, s_lo * nw)
+    t = timed(ms, reps=3)
+    d = sharding.digest_words(w[: (hi - lo) * MS_WORDS], lo * MS_WORDS)
     sharding.allreduce_sum_(d)
-    side["multistream_words"] = {"config": "configs[4]: 1e8 Philox streams x 256 words per GPU",
-                                 "seconds": round(t, 4), "gwords_s": round(n_str * nw * world / t / 1e9, 2),
-                                 "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / pk["hbm_gbs"], 3),
-                                 "digest": f"{int(d.item()) & 0xFFFFFFFFFFFFFFFF:016x}"}
+    ms_digest = f"{int(d.item()) & 0xFFFFFFFFFFFFFFFF:016x}"
+    ref4 = gold.get("cfg4_fullsize", {}).get("philox") if k == 1 else None
+    cr = _lib.curand_lib()
+    t_cu = timed(lambda: _lib.check(0 if cr.cbrng_curand_rows(lo, hi - lo, MS_WORDS, w.data_ptr(), sptr) == 0 else -3,
+                                    "curand rows"), reps=3)
+    words_s = MS_STREAMS * MS_WORDS / t / world
+    side["multistream_words"] = {
+        "config": f"configs[4]: 1e8 Philox streams x 256 words in total, stream-range shards over {world} GPU(s)",
+        "scaling": "strong",
+        "seconds": round(t, 4), "gwords_s": round(MS_STREAMS * MS_WORDS / t / 1e9, 2),
+        "roofline": roofline_of(work_or_none(sass_pipes.rows_work, 0, 0), words_s, 4, pk, sms, mhz),
+        "curand_rows": {"seconds": round(t_cu, 4), "gwords_s": round(MS_STREAMS * MS_WORDS / t_cu / 1e9, 2),
+                        "api": "device API: curand_init(seed = stream, 0, 0) + curand4, one thread per stream"},
+        "speedup_vs_curand": round(t_cu / t, 3),
+        "digest": ms_digest, "reference_digest": ref4,
+        "oracle_note": "reference_digest: the reference package's own prefix_words over all 1e8 x 256 words "
+                       "(tests/golden/make_golden_r2.py)",
+        "gpu_count_invariant": (ms_digest == ref4) if ref4 else None,
+        "matches_reference_fullsize": (ms_digest == ref4) if ref4 else None,
+    }
     del w
     torch.cuda.empty_cache()
 

@@ -359,3 +359,120 @@ uint64_t orc_brownian_checksum(uint64_t n, const uint64_t *pid, const double *x,
     }
     return h;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Full-size checks (tests/test_gpu_fullsize.py). Not reference functions: the
+ * order-free position-aware digest sum_i mix64(mix64(i) ^ w_i) mod 2^64 that
+ * the GPU side computes (paper_2310_19925_b200/sharding.py), streamed over the
+ * reference's outputs without materialising them, and the Box-Muller error of
+ * a device array against the reference's formula.                            */
+
+static inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static inline uint32_t f32_bits_of_word(uint32_t w) {
+    /* distributions.py:105-107 */
+    float f = (float)((double)(w >> 8) * 0x1p-24);
+    uint32_t b;
+    memcpy(&b, &f, 4);
+    return b;
+}
+
+/* Digest of words (as_f32 = 0) or of their uniform f32 bit patterns (as_f32 = 1)
+ * at stream word positions [word0, word0 + n) of stream (seed, sc) — the values
+ * uniform_f32_array / words would return for a generator positioned at word0
+ * (bulk.py:223-281; block counter = word0 / 4 for Philox/Threefry, = word0 for
+ * Squares, wrapping mod 2^32) — with global index offset `index0`. */
+uint64_t orc_digest_stream(int alg, uint64_t seed, uint32_t sc, uint64_t word0, uint64_t n, uint64_t index0,
+                           int as_f32) {
+    if (alg < 0 || alg > 2) return 0;
+    if (alg == ALG_SQUARES) seed &= M32;
+    const uint64_t key = orc_squares_key(seed);
+    uint64_t acc = 0;
+    const int64_t nchunks = (int64_t)((n + 4095) / 4096);
+#pragma omp parallel for schedule(static) reduction(+ : acc)
+    for (int64_t c = 0; c < nchunks; c++) {
+        const uint64_t lo = (uint64_t)c * 4096, k = n - lo < 4096 ? n - lo : 4096;
+        uint32_t blk[4];
+        uint64_t have = ~0ull;  /* block index held in blk */
+        for (uint64_t i = 0; i < k; i++) {
+            const uint64_t pos = word0 + lo + i;
+            uint32_t w;
+            if (alg == ALG_SQUARES) {
+                w = orc_squares_round(key, ((uint64_t)sc << 32) | (uint32_t)pos);
+            } else {
+                if ((pos >> 2) != have) {
+                    have = pos >> 2;
+                    block_of(alg, seed, sc, (uint32_t)have, blk);
+                }
+                w = blk[pos & 3];
+            }
+            if (as_f32) w = f32_bits_of_word(w);
+            acc += mix64(mix64(index0 + lo + i) ^ (uint64_t)w);
+        }
+    }
+    return acc;
+}
+
+/* Digest of prefix_words(alg, arange(seed_base, seed_base + n_streams), ctr, nwords)
+ * (bulk.py:162-207), optionally as uniform f32 bits; index i = stream * nwords + j
+ * counted from index0. */
+uint64_t orc_digest_prefix(int alg, uint64_t seed_base, uint64_t n_streams, uint32_t ctr, uint32_t nwords,
+                           uint64_t index0, int as_f32) {
+    if (alg < 0 || alg > 3 || nwords > 4096) return 0;
+    uint64_t acc = 0;
+#pragma omp parallel for schedule(static) reduction(+ : acc)
+    for (int64_t s = 0; s < (int64_t)n_streams; s++) {
+        uint32_t row[4096];
+        uint64_t seed = seed_base + (uint64_t)s;
+        if (alg == ALG_SQUARES) seed &= M32;
+        orc_words(alg, seed, ctr, 0, 0, nwords, row, NULL);
+        for (uint32_t j = 0; j < nwords; j++) {
+            const uint32_t w = as_f32 ? f32_bits_of_word(row[j]) : row[j];
+            acc += mix64(mix64(index0 + (uint64_t)s * nwords + j) ^ (uint64_t)w);
+        }
+    }
+    return acc;
+}
+
+/* Box-Muller error of device results z0/z1 for pairs [0, n_pairs) of stream
+ * (seed, sc) starting at block bc0 (one 4-word block per pair, distributions.py:
+ * 72-81, 110-120, libm as the reference's scalar normal2): out[0] = max error in
+ * units of ulp(max(|z|, 1)) (the parity tolerance's unit), out[1] = max error in
+ * ulps of z itself (z != 0), out[2] = count of values above `tol` units.
+ * Philox/Threefry only (the long-stream layout of configs[3]). */
+int orc_normal2_error(int alg, uint64_t seed, uint32_t sc, uint32_t bc0, uint64_t n_pairs, const double *z0,
+                      const double *z1, double tol, double out[3]) {
+    if (alg != ALG_PHILOX && alg != ALG_THREEFRY) return -1;
+    const double two_pi = 2.0 * M_PI;
+    double m_abs = 0.0, m_rel = 0.0, over = 0.0;
+#pragma omp parallel for schedule(static) reduction(max : m_abs, m_rel) reduction(+ : over)
+    for (int64_t i = 0; i < (int64_t)n_pairs; i++) {
+        uint32_t q[4];
+        block_of(alg, seed, sc, (uint32_t)(bc0 + (uint64_t)i), q);
+        const uint64_t a = (uint64_t)q[0] | ((uint64_t)q[1] << 32);
+        const uint64_t b = (uint64_t)q[2] | ((uint64_t)q[3] << 32);
+        const double u1 = 1.0 - (double)(a >> 11) * 0x1p-53;
+        const double u2 = (double)(b >> 11) * 0x1p-53;
+        const double r = sqrt(-2.0 * log(u1));
+        const double t = two_pi * u2;
+        const double ref[2] = {r * cos(t), r * sin(t)};
+        const double got[2] = {z0[i], z1[i]};
+        for (int k = 0; k < 2; k++) {
+            const double d = fabs(got[k] - ref[k]);
+            const double ua = d / (nextafter(fmax(fabs(ref[k]), 1.0), INFINITY) - fmax(fabs(ref[k]), 1.0));
+            if (ua > m_abs) m_abs = ua;
+            if (ua > tol) over += 1.0;
+            if (ref[k] != 0.0) {
+                const double ar = fabs(ref[k]);
+                const double ur = d / (nextafter(ar, INFINITY) - ar);
+                if (ur > m_rel) m_rel = ur;
+            }
+        }
+    }
+    out[0] = m_abs; out[1] = m_rel; out[2] = over;
+    return 0;
+}

@@ -60,6 +60,12 @@ def lib():
         L.orc_fnv1a64.restype = C.c_uint64
         L.orc_brownian_checksum.argtypes = [C.c_uint64, u64p, f64p, f64p, f64p, f64p]
         L.orc_brownian_checksum.restype = C.c_uint64
+        L.orc_digest_stream.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]
+        L.orc_digest_stream.restype = C.c_uint64
+        L.orc_digest_prefix.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, C.c_int]
+        L.orc_digest_prefix.restype = C.c_uint64
+        L.orc_normal2_error.argtypes = [C.c_int, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint64, f64p, f64p,
+                                        C.c_double, f64p]
         L.orc_num_threads.restype = C.c_int
         L.orc_set_num_threads.argtypes = [C.c_int]
         _lib = L
@@ -242,3 +248,33 @@ def brownian_checksum(x, y, vx, vy, pid: np.ndarray | None = None) -> int:
     arrs = [np.ascontiguousarray(a, np.float64) for a in (x, y, vx, vy)]
     pp = None if pid is None else np.ascontiguousarray(pid, np.uint64)
     return int(lib().orc_brownian_checksum(arrs[0].size, _p(pp, C.c_uint64), *(_p(a, C.c_double) for a in arrs)))
+
+
+# ---------------------------------------------------------------------------
+# Full-size checks (tests/test_gpu_fullsize.py): streamed digests and the
+# Box-Muller error of a device array, never materialising the reference output.
+# ---------------------------------------------------------------------------
+
+def digest_stream(alg, seed: int, sc: int, word0: int, n: int, index0: int = 0, as_f32: bool = False) -> int:
+    """sum_i mix64(mix64(index0 + i) ^ v_i) mod 2^64 over words (or their uniform f32 bit
+    patterns) at positions [word0, word0 + n) of stream (seed, sc) (bulk.py:223-281)."""
+    return int(lib().orc_digest_stream(_alg(alg), seed, sc, word0, n, index0, int(as_f32)))
+
+
+def digest_prefix(alg, seed_base: int, n_streams: int, ctr: int, nwords: int, index0: int = 0,
+                  as_f32: bool = False) -> int:
+    """The same digest over prefix_words(alg, arange(seed_base, ...), ctr, nwords) (bulk.py:162-207)."""
+    return int(lib().orc_digest_prefix(_alg(alg), seed_base, n_streams, ctr, nwords, index0, int(as_f32)))
+
+
+def normal2_error(alg, seed: int, sc: int, bc0: int, z0: np.ndarray, z1: np.ndarray, tol: float = 4.0) -> dict:
+    """Error of device Box-Muller pairs against the reference formula (distributions.py:72-81):
+    max in ulp(max(|z|, 1)), max in ulps of z, and the count above `tol`."""
+    z0 = np.ascontiguousarray(z0, np.float64)
+    z1 = np.ascontiguousarray(z1, np.float64)
+    out = np.zeros(3, np.float64)
+    rc = lib().orc_normal2_error(_alg(alg), seed, sc, bc0, z0.size, _p(z0, C.c_double), _p(z1, C.c_double), tol,
+                                 _p(out, C.c_double))
+    if rc:
+        raise ValueError("normal2_error: Philox/Threefry only")
+    return {"max_units": float(out[0]), "max_rel_ulps": float(out[1]), "over_tol": int(out[2])}

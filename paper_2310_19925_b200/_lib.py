@@ -81,6 +81,7 @@ CURAND_SIGNATURES = {
     "cbrng_curand_brownian_init": (i32, [vp, u64, vp, vp, vp, vp, vp]),
     "cbrng_curand_brownian_steps": (i32, [vp, u64, vp, vp, vp, vp, u64, f64, f64, f64, i32, vp]),
     "cbrng_probe_store": (i32, [vp, u64, i32, i32, vp]),
+    "cbrng_curand_rows": (i32, [u64, u64, u32, vp, vp]),
 }
 
 

@@ -10,7 +10,8 @@
 //     state loaded and stored every step. Same SoA particle layout and update
 //     arithmetic as the product kernel, so only the RNG strategy differs.
 //   * a stronger cuRAND variant for the time-fused comparison: the state is
-//     loaded once, kept in registers for all steps, and stored once.
+//     loaded once, kept in registers for all steps, and stored once;
+//   * configs[4]'s many-stream shape through the device API (curand_rows_kernel).
 // cuRAND's double map differs from the reference's (curand_uniform.h), so these
 // results are not parity-checked — they only time the same work.
 #include <cmath>
@@ -133,6 +134,28 @@ int cbrng_curand_brownian_steps(void *state, uint64_t n, double *x, double *y, d
 }
 
 }  // extern "C"
+
+// configs[4] shape with the cuRAND device API: stream s = curand_init(seed = s,
+// subsequence 0, offset 0) on a Philox4_32_10 state in registers, 256 words
+// drawn with curand4 and written row-major (out[s][j]), one thread per stream,
+// 16-byte stores. What a cuRAND user writes for "n independent streams x 256".
+__global__ void __launch_bounds__(256) curand_rows_kernel(uint64_t seed_base, uint64_t n_streams, uint32_t nwords,
+                                                          uint4 *out) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n_streams) return;
+    curandStatePhilox4_32_10_t st;
+    curand_init(seed_base + s, 0, 0, &st);
+    uint4 *row = out + s * (nwords / 4);
+    for (uint32_t j = 0; j < nwords / 4; j++) __stcs(row + j, curand4(&st));
+}
+
+extern "C" int cbrng_curand_rows(uint64_t seed_base, uint64_t n_streams, uint32_t nwords, uint32_t *out,
+                                 void *stream) {
+    if (nwords % 4) return -1;
+    const uint64_t grid = (n_streams + 255) / 256;
+    curand_rows_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(seed_base, n_streams, nwords, (uint4 *)out);
+    return cudaGetLastError() == cudaSuccess ? 0 : -3;
+}
 
 // ---------------------------------------------------------------------------
 // Store-bandwidth probe (measurement only): the write-only HBM ceiling for the

@@ -298,7 +298,7 @@ class Generator:
         return bulk.generator_words(self, n, out=out, device=device)
 
     def copy(self) -> "Generator":
-        g = Generator.__new__(Generator)
+        g = type(self).__new__(type(self))
         for name in Generator.__slots__:
             setattr(g, name, getattr(self, name))
         return g
@@ -312,7 +312,12 @@ class Generator:
     def from_state_bytes(cls, data: bytes) -> "Generator":
         """generators.py:355-374"""
         tag, seed, stream_ctr, block_ctr, cache_pos = STATE_STRUCT.unpack(data)
-        g = cls(Algorithm(tag), seed, stream_ctr)
+        g = Generator(Algorithm(tag), seed, stream_ctr)
+        if cls is not Generator:  # Philox.from_state_bytes(...) etc.: same engine, the subclass's type
+            fixed = getattr(cls, "ALGORITHM", None)
+            if fixed is not None and fixed is not g.algorithm:
+                raise ValueError(f"state is for {g.algorithm.name.lower()}, not {fixed.name.lower()}")
+            g.__class__ = cls
         if g.words_per_block == 1:
             if cache_pos != 0:
                 raise ValueError("cache position must be 0 for single-word algorithms")
@@ -350,6 +355,7 @@ class Philox(Generator):
     """Philox4x32-10 stream (seed, counter): the OpenRAND `Philox` generator class."""
 
     __slots__ = ()
+    ALGORITHM = Algorithm.PHILOX
 
     def __init__(self, seed: int, counter: int = 0):
         super().__init__(Algorithm.PHILOX, seed, counter)
@@ -357,6 +363,7 @@ class Philox(Generator):
 
 class Threefry(Generator):
     __slots__ = ()
+    ALGORITHM = Algorithm.THREEFRY
 
     def __init__(self, seed: int, counter: int = 0):
         super().__init__(Algorithm.THREEFRY, seed, counter)
@@ -364,6 +371,7 @@ class Threefry(Generator):
 
 class Squares(Generator):
     __slots__ = ()
+    ALGORITHM = Algorithm.SQUARES
 
     def __init__(self, seed: int, counter: int = 0):
         super().__init__(Algorithm.SQUARES, seed, counter)
@@ -371,6 +379,7 @@ class Squares(Generator):
 
 class Tyche(Generator):
     __slots__ = ()
+    ALGORITHM = Algorithm.TYCHE
 
     def __init__(self, seed: int, counter: int = 0):
         super().__init__(Algorithm.TYCHE, seed, counter)

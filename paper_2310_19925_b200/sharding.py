@@ -42,6 +42,12 @@ def shard_range(n: int, rank: int, world: int, align: int = 1) -> tuple[int, int
     return min(lo_u * align, n), min(hi_u * align, n)
 
 
+def words_per_stream(alg) -> int:
+    """Words one stream holds before its counter wraps: 2^32 blocks x 4 words
+    (Philox/Threefry) or 2^32 words (Squares)."""
+    return 1 << 32 if as_algorithm(alg) is Algorithm.SQUARES else 1 << 34
+
+
 def stream_segments(lo: int, hi: int, per_stream: int = PAIRS_PER_STREAM):
     """Split global element range [lo, hi) into (stream_offset, first_index_in_stream, count) pieces."""
     out = []
@@ -66,6 +72,23 @@ def normal2_long(alg, seed: int, ctr0: int, lo: int, hi: int, z0: torch.Tensor, 
     for s, off, k in stream_segments(lo, hi, per_stream):
         _lib.check(lib.cbrng_normal2_f64(int(alg), seed, (ctr0 + s) & MASK32, 4 * off, None, k,
                                          z0[pos:].data_ptr(), z1[pos:].data_ptr(), None, st), "normal2")
+        pos += k
+
+
+def uniform_f32_long(alg, seed: int, ctr0: int, lo: int, hi: int, out: torch.Tensor) -> None:
+    """Values [lo, hi) of the long-stream uniform f32 layout into `out` (device, len hi-lo):
+    value i is word i mod P of stream (seed, ctr0 + i // P), P = words_per_stream(alg),
+    so a range past one stream's period continues on the next stream counter instead of
+    wrapping onto values already produced (README.md:23-24)."""
+    alg = as_algorithm(alg)
+    if alg is Algorithm.TYCHE:
+        raise ValueError("Tyche is serial; the long-stream layout needs a counter-based algorithm")
+    lib = _lib.lib()
+    st = _dev.sptr(out)
+    pos = 0
+    for s, off, k in stream_segments(lo, hi, words_per_stream(alg)):
+        _lib.check(lib.cbrng_uniform_f32(int(alg), seed, (ctr0 + s) & MASK32, off, None, k, out[pos:].data_ptr(),
+                                         None, st), "uniform_f32")
         pos += k
 
 

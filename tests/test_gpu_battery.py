@@ -105,3 +105,66 @@ def test_emit_cli_exit_codes(st):
     from paper_2310_19925_b200 import emit
 
     assert emit.main(["--gen", "nope", "--n", "4"]) == 2
+
+
+# ---- foreign word sources: the reference's sabotage fixtures (fixtures.py:17-60),
+# restated here as test infrastructure; the battery must take any word source
+# (stats.py:289-318) and fail these exactly as the reference's battery does.
+class _Constant:
+    name, seed_bits = "constant", 64
+
+    def stream_words(self, seed, stream_counter, n):
+        return np.zeros(n, dtype=np.uint32)
+
+    def prefix_words(self, seeds, stream_counters, nwords):
+        n = np.broadcast_shapes(np.shape(np.atleast_1d(seeds)), np.shape(np.atleast_1d(stream_counters)))[0]
+        return np.zeros((n, nwords), dtype=np.uint32)
+
+
+class _CounterEcho:
+    name, seed_bits = "counter-echo", 64
+
+    def stream_words(self, seed, stream_counter, n):
+        return (np.arange(n, dtype=np.uint64) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+
+    def prefix_words(self, seeds, stream_counters, nwords):
+        n = np.broadcast_shapes(np.shape(np.atleast_1d(seeds)), np.shape(np.atleast_1d(stream_counters)))[0]
+        return np.broadcast_to(np.arange(nwords, dtype=np.uint32), (n, nwords)).copy()
+
+
+class _LowBitStuck:
+    """A healthy Philox source (here: this package's own) with output bit 0 wedged at 1."""
+
+    name, seed_bits = "low-bit-stuck", 64
+
+    def __init__(self):
+        from paper_2310_19925_b200.bulk import AlgorithmSource
+        from paper_2310_19925_b200.generators import Algorithm
+
+        self._inner = AlgorithmSource(Algorithm.PHILOX)
+
+    def stream_words(self, seed, stream_counter, n):
+        return np.asarray(self._inner.stream_words(seed, stream_counter, n)) | np.uint32(1)
+
+    def prefix_words(self, seeds, stream_counters, nwords):
+        return np.asarray(self._inner.prefix_words(seeds, stream_counters, nwords)) | np.uint32(1)
+
+
+@pytest.mark.parametrize("name,cls", [("constant", _Constant), ("counter-echo", _CounterEcho),
+                                      ("low-bit-stuck", _LowBitStuck)])
+def test_run_battery_foreign_sources(st, name, cls):
+    """Reports equal the reference battery's on its own sabotage fixtures
+    (tests/golden/golden_r2.json, make_golden_r2.py)."""
+    import json
+
+    from conftest import GOLDEN_DIR
+
+    ref = json.loads((GOLDEN_DIR / "golden_r2.json").read_text())["battery_sabotage_16MiB"][name]
+    got = [st.report_to_dict(r) for r in st.run_battery(cls(), 16 * 2**20)]
+    assert [g["test_name"] for g in got] == [r["test_name"] for r in ref]
+    for g, r in zip(got, ref):
+        assert g["verdict"] == r["verdict"] and g["n_samples"] == r["n_samples"], g["test_name"]
+        for k in ("statistic", "p_value_or_z"):
+            a, b = g[k], r[k]
+            assert (math.isnan(a) and math.isnan(b)) or math.isclose(a, b, rel_tol=1e-9, abs_tol=1e-12), (g, r)
+    assert not st.battery_passes(st.run_battery(cls(), 16 * 2**20))

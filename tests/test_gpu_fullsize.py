@@ -1,0 +1,135 @@
+"""Full-size parity at every BASELINE config on one B200.
+
+Every value of the workload is checked, not a sample:
+  * configs[1]: the four 2^30-value uniform f32 fills (Philox / Threefry / Squares
+    single stream seed 42 ctr 0; Tyche 2^22 streams x 256) — position-aware
+    digest over all 2^30 values against the digest the reference package itself
+    produced over its own outputs (tests/golden/make_golden_r2.py,
+    distributions.py:105-107, bulk.py:162-207);
+  * configs[4]: 10^8 Philox streams x 256 words — the same digest against the
+    reference package's prefix_words over all 2.56e10 words;
+  * configs[3]: all 2^34 Box-Muller values (2^33 pairs, long-stream layout)
+    against the reference formula on the host (glibc libm, distributions.py:72-81,
+    110-120): the largest error over every value, in ulp(max(|z|, 1)) (the stated
+    tolerance's unit, bound 4) and in ulps of z itself;
+  * configs[2]: the 10M x 10k fused walk, 1024 pids replayed by the oracle for all
+    10k steps, bit for bit.
+Digest: sum_i mix64(mix64(i) ^ v_i) mod 2^64 (sharding.digest_words), which any
+sharding of the array reproduces (tests/test_sharding.py).
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_DIR
+
+pytestmark = pytest.mark.gpu
+
+M64 = (1 << 64) - 1
+
+
+@pytest.fixture(scope="module")
+def cb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2310_19925_b200 as cb
+
+    return cb
+
+
+@pytest.fixture(scope="module")
+def g2():
+    return json.loads((GOLDEN_DIR / "golden_r2.json").read_text())
+
+
+def _hex(t) -> str:
+    return f"{int(t.item()) & M64:016x}"
+
+
+@pytest.mark.parametrize("alg", ["philox", "threefry", "squares", "tyche"])
+def test_cfg1_every_value_matches_reference(cb, g2, alg):
+    import torch
+    from paper_2310_19925_b200 import bulk, sharding
+
+    n = 1 << 30
+    if alg == "tyche":
+        out = bulk.prefix_uniform_f32("tyche", range(1 << 22), 0, 256)
+    else:
+        out = cb.uniform_f32_array(cb.make_generator(alg, 42, 0), n)
+    got = _hex(sharding.digest_words(out.view(torch.uint32), 0))
+    del out
+    torch.cuda.empty_cache()
+    assert got == g2["cfg1_fullsize"]["values"][alg]
+
+
+def test_cfg4_every_word_matches_reference(cb, g2):
+    """1e8 x 256 Philox words, generated in 10 slabs of 1e7 streams (10 GB each)."""
+    import torch
+    from paper_2310_19925_b200 import _dev, _lib, sharding
+
+    n, nw, slab = 100_000_000, 256, 10_000_000
+    buf = torch.empty(slab * nw, dtype=torch.uint32, device="cuda")
+    acc = torch.zeros(1, dtype=torch.int64, device="cuda")
+    lib = _lib.lib()
+    for lo in range(0, n, slab):
+        k = min(slab, n - lo)
+        _lib.check(lib.cbrng_prefix_words(0, None, lo, None, 0, k, nw, buf.data_ptr(), _dev.sptr(buf)), "prefix")
+        sharding.digest_words(buf[: k * nw], lo * nw, acc)
+    got = _hex(acc)
+    del buf
+    torch.cuda.empty_cache()
+    assert got == g2["cfg4_fullsize"]["philox"]
+
+
+def test_cfg3_every_value_within_tolerance(cb, oracle):
+    """All 2^33 pairs of the long-stream layout (pair i: stream (42, i div 2^32),
+    block i mod 2^32), compared on the host against the reference formula in
+    chunks of 2^28 pairs. Bound: 4 ulp(max(|z|, 1)) per value."""
+    import torch
+    from paper_2310_19925_b200 import sharding
+
+    total, chunk = 1 << 33, 1 << 28
+    z0 = torch.empty(chunk, dtype=torch.float64, device="cuda")
+    z1 = torch.empty(chunk, dtype=torch.float64, device="cuda")
+    h0 = torch.empty(chunk, dtype=torch.float64, pin_memory=True)
+    h1 = torch.empty(chunk, dtype=torch.float64, pin_memory=True)
+    worst = {"max_units": 0.0, "max_rel_ulps": 0.0, "over_tol": 0}
+    for lo in range(0, total, chunk):
+        sharding.normal2_long("philox", 42, 0, lo, lo + chunk, z0, z1)
+        h0.copy_(z0)
+        h1.copy_(z1)
+        s, off = divmod(lo, sharding.PAIRS_PER_STREAM)
+        e = oracle.normal2_error("philox", 42, s, off, h0.numpy(), h1.numpy(), tol=4.0)
+        worst = {"max_units": max(worst["max_units"], e["max_units"]),
+                 "max_rel_ulps": max(worst["max_rel_ulps"], e["max_rel_ulps"]),
+                 "over_tol": worst["over_tol"] + e["over_tol"]}
+    del z0, z1
+    torch.cuda.empty_cache()
+    print("configs[3] 2^34 values:", json.dumps(worst))
+    assert worst["over_tol"] == 0 and worst["max_units"] <= 4.0, worst
+
+
+def test_cfg2_full_walk_1024_pids(cb, oracle):
+    """configs[2] at full size (10M particles x 10k steps, fused), 1024 pids spread
+    over the range (both ends included) replayed by the oracle for all 10k steps."""
+    n, steps = 10_000_000, 10_000
+    cfg = cb.SimConfig(n, steps)
+    p = cb.init_particles(cfg)
+    cb.brownian.run_steps(p, cfg)
+    rng = np.random.default_rng(11)
+    pids = np.unique(np.concatenate([[0, 1, 255, 256, n // 2, n - 2, n - 1],
+                                     rng.integers(0, n, 1100)]))[:1024].astype(np.uint64)
+    pids[-1] = n - 1
+    pids = np.unique(pids)
+    assert pids.size >= 1000
+    ref = oracle.brownian_init("philox", pids.size, 0, pid=pids)
+    oracle.brownian_steps("philox", ref, 1, steps, pid=pids)
+    idx = pids.astype(np.int64)
+    for got, r in zip((p.x, p.y, p.vx, p.vy), ref):
+        assert np.array_equal(got.cpu().numpy()[idx], r)

@@ -235,3 +235,42 @@ class TestBatteryHostFormulas:
         assert st.classify_p(1e-7) is st.Verdict.FAIL
         assert st.classify_p(1 - 1e-7, folded=True) is st.Verdict.PASS
         assert st.classify_p(float("nan")) is st.Verdict.FAIL
+
+
+def test_oracle_fullsize_cfg1_digests_match_reference():
+    """The oracle's streamed digests over all 2^30 values of configs[1] equal the
+    digests of the reference package's own outputs (make_golden_r2.py) — the
+    oracle is pinned at full size, not only on short vectors."""
+    import json
+
+    from conftest import GOLDEN_DIR
+    from oracle import oracle as orc
+
+    ref = json.loads((GOLDEN_DIR / "golden_r2.json").read_text())["cfg1_fullsize"]["values"]
+    for alg in ("philox", "squares"):
+        assert f"{orc.digest_stream(alg, 42, 0, 0, 1 << 30, as_f32=True):016x}" == ref[alg], alg
+    assert f"{orc.digest_prefix('tyche', 0, 1 << 22, 0, 256, as_f32=True):016x}" == ref["tyche"]
+
+
+def test_oracle_digest_matches_numpy_definition():
+    from oracle import oracle as orc
+    from paper_2310_19925_b200 import sharding
+
+    for alg in ("philox", "threefry", "squares"):
+        w = orc.stream_words(alg, 9, 4, 5000)
+        assert orc.digest_stream(alg, 9, 4, 0, 5000) == sharding.digest_words_np(w, 0)
+        assert orc.digest_stream(alg, 9, 4, 1001, 3999, 1001) == sharding.digest_words_np(w[1001:], 1001)
+        f = orc.words_to_f32(w).view(np.uint32)
+        assert orc.digest_stream(alg, 9, 4, 0, 5000, as_f32=True) == sharding.digest_words_np(f, 0)
+    w = orc.prefix_words_arange("tyche", 3, 100, 1, 256)
+    assert orc.digest_prefix("tyche", 3, 100, 1, 256, 77) == sharding.digest_words_np(w.reshape(-1), 77)
+
+
+def test_oracle_normal2_error_zero_on_itself():
+    from oracle import oracle as orc
+
+    z0, z1 = orc.normal2("threefry", 5, 2, 10_000)
+    e = orc.normal2_error("threefry", 5, 2, 0, z0, z1)
+    assert e == {"max_units": 0.0, "max_rel_ulps": 0.0, "over_tol": 0}
+    z0[7] = np.nextafter(z0[7], np.inf)
+    assert orc.normal2_error("threefry", 5, 2, 0, z0, z1)["max_units"] > 0

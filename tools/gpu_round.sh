@@ -4,12 +4,12 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu.txt 2>&1
 nproc > gpurun_out/nproc.txt
-timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -p no:cacheprovider -rs > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 2400 python -m pytest tests -m gpu -q --timeout 900 ${PYTEST_ARGS:-} -s --durations=25 -p no:cacheprovider -rs > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python bench.py ${BENCH_ARGS:---steps 50 --warmup 3} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 900 python bench.py ${BENCH_ARGS:---steps 20 --warmup 5} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
 if [ -n "$DO_MULTI" ]; then
-  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 \
-      bench.py --gpus 2 --steps 5 --warmup 3 --quick --dist-backend gloo > gpurun_out/bench_2rank.json 2> gpurun_out/bench_2rank.err
+  timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 --dist-backend gloo --no-cpu \
+      > gpurun_out/bench_2rank.json 2> gpurun_out/bench_2rank.err
   echo "2rank rc=$?" >> gpurun_out/bench_2rank.err
   timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 fi
