@@ -144,10 +144,10 @@ class _LowBitStuck:
         self._inner = AlgorithmSource(Algorithm.PHILOX)
 
     def stream_words(self, seed, stream_counter, n):
-        return np.asarray(self._inner.stream_words(seed, stream_counter, n)) | np.uint32(1)
+        return np.asarray(self._inner.stream_words(seed, stream_counter, n, device="cpu")) | np.uint32(1)
 
     def prefix_words(self, seeds, stream_counters, nwords):
-        return np.asarray(self._inner.prefix_words(seeds, stream_counters, nwords)) | np.uint32(1)
+        return np.asarray(self._inner.prefix_words(seeds, stream_counters, nwords, device="cpu")) | np.uint32(1)
 
 
 @pytest.mark.parametrize("name,cls", [("constant", _Constant), ("counter-echo", _CounterEcho),
