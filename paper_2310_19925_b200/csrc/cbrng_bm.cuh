@@ -25,8 +25,8 @@
 //         r = z - 1 is exact and ln u1 keeps full relative accuracy as u1 -> 1.
 //   sqrt: MUFU.RSQ64H seed, one Newton step for sqrt, one residual
 //         correction with the seed's 1/(2 sqrt): 7 ops.
-//   t:    (2 pi 2^-53) * f64(u2 bits): the same rounded value as (2 pi) * u2
-//         (scaling by 2^-53 is exact on both sides), one DMUL.
+//   t:    (2 pi 2^-64) * f64(u2 2^11): the same rounded value as (2 pi) * u2
+//         (scaling by powers of two is exact on both sides), one DMUL.
 //   sincos: table point j = round(128 u2) from the integer u2, reduction by
 //         j pi/64, short Taylor sin/cos on |x| <= pi/128 and the angle sum with
 //         a 129-entry {sin, cos}(j pi/64) table: 14 ops.
@@ -40,11 +40,12 @@ namespace cbrng {
 struct BmConst {
     double m2ln2_hi, m2ln2_lo;  // -2 ln2 split: ln2_hi a multiple of 2^-43
     double two_pi_2m53;         // (2 pi) * 2^-53, exact scaling of the rounded 2*math.pi
+    double two_pi_2m64;         // (2 pi) * 2^-64
 };
 
 __constant__ BmConst c_bm = {
     -2.0 * 0x1.62e42fefa3800p-1, -2.0 * 0x1.ef35793c7673p-45,
-    6.283185307179586 * 0x1p-53,
+    6.283185307179586 * 0x1p-53, 6.283185307179586 * 0x1p-64,
 };
 
 // {-2 invc, -2 logc hi, -2 logc lo, 0} per subinterval (tools/gen_logtab.py).
@@ -82,12 +83,12 @@ __device__ __forceinline__ double u64_to_f64_xu(uint64_t v) {
     return d;
 }
 
-// -2 ln(v 2^-53) for an integer v in [1, 2^53].
-__device__ __forceinline__ double bm_m2log(uint64_t v, const double4 *tab) {
-    const double dv = u64_to_f64_xu(v);  // exact: v < 2^54
+// -2 ln(dv 2^-E) for dv = v 2^(E-53), v an integer in [1, 2^53] (dv exact).
+template <int E = 53>
+__device__ __forceinline__ double bm_m2log_d(double dv, const double4 *tab) {
     const uint32_t hi = (uint32_t)__double2hiint(dv);
     const uint32_t th = hi - 0x3fe60000u;            // bits(dv) - bits(0.6875); the low word of OFF is 0
-    const int k = ((int)th >> 20) - 53;              // dv = 2^(k+53) z
+    const int k = ((int)th >> 20) - E;               // dv = 2^(k+E) z
     const uint32_t i = (th >> 12) & 255u;            // top 8 mantissa bits of bits(dv) - OFF
     const double z = __hiloint2double((int)(hi - (th & 0xfff00000u)), __double2loint(dv));
     const double4 e = tab[i];
@@ -101,6 +102,7 @@ __device__ __forceinline__ double bm_m2log(uint64_t v, const double4 *tab) {
     const double q = fma(s * s, p, s);
     return w + fma(kd, c_bm.m2ln2_lo, q + e.z);
 }
+
 
 // sqrt(a), a >= 0 finite. a = 0 (u1 == 1) must give 0: the rsqrt input is
 // clamped to the smallest normal on the high word (one integer max, no FP
@@ -123,8 +125,9 @@ __device__ __forceinline__ double bm_sqrt(double a) {
 // sum with the table's sin/cos of j pi/64, which are exact zeros and ones at
 // the multiples of pi/2, so results next to a zero keep their relative
 // accuracy. 14 FP64 ops (the fdlibm-kernel form with a pi/2 reduction: 18).
-__device__ __forceinline__ void sincos_2pi(double t, uint64_t v, const double2 *sct, double &sn, double &cs) {
-    const int j = (int)((v + (1ull << 45)) >> 46);  // 0..128
+__device__ __forceinline__ void sincos_2pi(double t, uint32_t w3, const double2 *sct, double &sn, double &cs) {
+    // j = round(128 u2) = (u2 + 2^45) >> 46 with u2 = (w3:w2) >> 11, from the high word alone
+    const int j = (int)(((w3 >> 24) + 1u) >> 1);  // 0..128
     const double jd = (double)j;
     double x = fma(-jd, CBRNG_PI64_HI, t);
     x = fma(-jd, CBRNG_PI64_LO, x);
@@ -140,12 +143,18 @@ __device__ __forceinline__ void sincos_2pi(double t, uint64_t v, const double2 *
 
 // One Box-Muller pair from one 4-word block; `tab` = the tables staged in shared
 // memory (bm_stage_table).
+//   With m = (w1:w0) with the low 11 bits cleared = u 2^11 (exact in f64),
+//   v 2^11 = (2^53 - u) 2^11 = 2^64 - m, a multiple of 2^11 in [2^11, 2^64]: one
+//   exact DADD. One LOP3 + I2F + DADD instead of two 64-bit shifts, a 64-bit
+//   subtract and the I2F; the log takes the 2^11 into its exponent.
+//   u2 2^11 = (w3:w2) with the low 11 bits cleared converts exactly, and
+//   (2 pi 2^-64) (u2 2^11) rounds exactly like (2 pi) (u2 2^-53).
 __device__ __forceinline__ void box_muller_fast(uint4 w, double &z0, double &z1, const BmTables *tab) {
-    const uint64_t u = (((uint64_t)w.y << 32) | w.x) >> 11;
-    const uint64_t u2 = (((uint64_t)w.w << 32) | w.z) >> 11;
-    const double r = bm_sqrt(bm_m2log((1ull << 53) - u, tab->log));
+    const uint64_t m1 = ((uint64_t)w.y << 32) | (w.x & 0xFFFFF800u);  // u 2^11
+    const uint64_t m2 = ((uint64_t)w.w << 32) | (w.z & 0xFFFFF800u);  // u2 2^11
+    const double r = bm_sqrt(bm_m2log_d<64>(__dsub_rn(0x1p64, u64_to_f64_xu(m1)), tab->log));
     double s, c;
-    sincos_2pi(c_bm.two_pi_2m53 * u64_to_f64_xu(u2), u2, tab->sc, s, c);
+    sincos_2pi(c_bm.two_pi_2m64 * u64_to_f64_xu(m2), w.w, tab->sc, s, c);
     z0 = __dmul_rn(r, c);
     z1 = __dmul_rn(r, s);
 }

@@ -208,6 +208,40 @@ __global__ void __launch_bounds__(256, MINB) brownian_fused_philox_kernel(const 
     if (live) { a.x[i] = x; a.y[i] = y; a.vx[i] = vx; a.vy[i] = vy; }
 }
 
+// The same walk with one step table per warp instead of per CTA: lane l
+// computes the step-uniform products of step base + l, the warp reads entry s
+// for step base + s (a broadcast LDS), and __syncwarp is the only
+// synchronisation, so warps of a CTA never wait for each other (the CTA-wide
+// table costs two __syncthreads per 256 steps: ncu r1zd "barrier" 2.0 cycles per
+// instruction, 12 % of the stall time). The table work grows from 1/256 to 1/32
+// of a step-uniform evaluation per particle-step (2 IMAD.WIDE / 32). Measured
+// 1 % slower than the CTA table (3.657e11 vs 3.691e11 p-steps/s): the barrier
+// stalls were not what bounds the walk (the FMA-heavy pipe at 63 %, dispatch
+// stalls). Tuning build only (CBRNG_BROWNIAN_TAB=2).
+template <bool FOLD, int MINB>
+__global__ void __launch_bounds__(256, MINB) brownian_fused_philox_wtab_kernel(const __grid_constant__ BrownArgs a) {
+    __shared__ uint4 tab[256 / 32][32];
+    uint4 *wt = tab[threadIdx.x >> 5];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = i < a.n;
+    const uint64_t pid = live ? (a.pid ? a.pid[i] : a.pid_base + i) : 0;
+    double x = 0.0, y = 0.0, vx = 0.0, vy = 0.0;
+    if (live) { x = a.x[i]; y = a.y[i]; vx = a.vx[i]; vy = a.vy[i]; }
+    const PhiloxParticle<true> P = philox_particle_setup<true>(pid);
+    const uint32_t ctr0 = a.init_ctr + (uint32_t)a.first_it;
+    const uint32_t nsteps = (uint32_t)a.nsteps;
+    for (uint32_t base = 0; base < nsteps; base += 32) {
+        __syncwarp();  // the previous chunk's entries are no longer read
+        wt[lane] = philox_step_uniform(ctr0 + base + lane);
+        __syncwarp();
+        const uint32_t m = nsteps - base < 32u ? nsteps - base : 32u;
+#pragma unroll 2
+        for (uint32_t s = 0; s < m; s++) step_update<FOLD>(x, y, vx, vy, philox_particle_block_u(P, wt[s]), a);
+    }
+    if (live) { a.x[i] = x; a.y[i] = y; a.vx[i] = vx; a.vy[i] = vy; }
+}
+
 // ---------------- deterministic statistics ----------------
 __device__ __forceinline__ int64_t fixq(double v, double scale) { return __double2ll_rn(v * scale); }
 
@@ -277,6 +311,8 @@ static bool brownian_pdl() {
     return v;
 }
 
+constexpr int BROWNIAN_TAB_DEFAULT = 1;
+
 // MINB applies to the fused table kernel; the per-step kernel keeps 5 CTAs/SM
 // (6 spills there).
 template <int ALG, bool HI0, bool FOLD, int MINB>
@@ -285,8 +321,12 @@ static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
     auto k = mode == CBRNG_BROWNIAN_PER_STEP && MINB > 1 ? brownian_steps_kernel<ALG, HI0, FOLD, (MINB > 4 ? 4 : MINB)>
                                                        : brownian_steps_kernel<ALG, HI0, FOLD, (MINB > 5 ? 5 : MINB)>;
     if constexpr (ALG == PHILOX && HI0) {
-        static const bool tab = tuning_knob("CBRNG_BROWNIAN_TAB", 1, 0, 1) != 0;
-        if (mode == CBRNG_BROWNIAN_FUSED && tab) k = brownian_fused_philox_kernel<FOLD, MINB>;
+        // step table: 0 none, 1 per CTA (brownian_fused_philox_kernel), 2 per warp
+        static const int tab = tuning_knob("CBRNG_BROWNIAN_TAB", BROWNIAN_TAB_DEFAULT, 0, 2);
+        if (mode == CBRNG_BROWNIAN_FUSED && tab == 1) k = brownian_fused_philox_kernel<FOLD, MINB>;
+        if constexpr (TUNING) {  // per-warp tables: 1 % slower (profiles/r2c_tune.md), tuning build only
+            if (mode == CBRNG_BROWNIAN_FUSED && tab == 2) k = brownian_fused_philox_wtab_kernel<FOLD, MINB>;
+        }
     }
     // One thread per particle: the fused kernel needs every particle resident
     // or queued, so the grid covers n (no persistence).

@@ -222,7 +222,115 @@ __global__ void __launch_bounds__(256) normal2_words_kernel(const uint4 *__restr
     }
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised Box-Muller fill (single stream, block-aligned).
+//
+// The fused form (fill_kernel<.., OUT_NORMAL, ..>) runs the Philox block (16
+// IMAD.WIDE + 18 LOP3: the FMA-heavy pipe) and the transform (35 FP64 ops) in
+// the same warp, so all warps alternate between a heavy-pipe phase and an
+// FP64 phase more or less in step and neither pipe is fed steadily (ncu r2a:
+// 63 % issue, math-pipe throttle and dispatch stalls on both phases). Here NP
+// producer warps generate the 4-word blocks of a tile of pairs into a
+// shared-memory ring and NC consumer warps turn them into (z0, z1) and store
+// them, so every SM sub-partition always has warps of both kinds ready.
+// Hand-off per stage: named barriers FULL[s] (producers arrive, consumers
+// wait) and EMPTY[s] (consumers arrive, producers wait), 16 B of shared
+// memory per pair each way.
+//
+// Layout: tile = NC*32*CI pairs. Consumer thread c owns pairs CI*c .. CI*c+CI-1
+// (16-byte stores of pair-adjacent z0 / z1 doubles); pair CI*c + k sits in
+// slot k*(NC*32) + c, so producer stores and consumer loads are both
+// conflict-free 128-bit accesses.
+template <int NP, int NC, int CI, int STAGES>
+struct BmWs {
+    static constexpr int THREADS = 32 * (NP + NC);
+    static constexpr int TILE = 32 * NC * CI;        // pairs per stage
+    static constexpr int PER_PRODUCER = TILE / (32 * NP);
+    static_assert(TILE % (32 * NP) == 0, "tile must split evenly over producers");
+    static_assert(CI % 2 == 0, "consumers store pair-adjacent 16-byte vectors");
+    struct Smem {
+        BmTables tab;
+        uint4 ring[STAGES][TILE];
+    };
+};
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int ALG, int V, int NP, int NC, int CI, int STAGES, int MB>
+__global__ void __launch_bounds__(BmWs<NP, NC, CI, STAGES>::THREADS, MB)
+    bm_ws_kernel(const __grid_constant__ FillArgs<ALG> a) {
+    using W = BmWs<NP, NC, CI, STAGES>;
+    __shared__ typename W::Smem sm;
+    bm_stage_table(&sm.tab);
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint64_t n_tiles = (a.n_units + W::TILE - 1) / W::TILE;
+    // barrier ids: 1 + s = FULL[s], 1 + STAGES + s = EMPTY[s] (0 is __syncthreads)
+    if (warp < NP) {
+        const uint32_t p = threadIdx.x;
+        uint32_t s = 0;
+        for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            if (t >= (uint64_t)STAGES * gridDim.x) named_bar_sync(1 + STAGES + s, W::THREADS);  // stage s consumed
+            uint4 w[W::PER_PRODUCER];
+#pragma unroll
+            for (int j = 0; j < W::PER_PRODUCER; j++) {
+                const uint32_t q = p + j * 32 * NP;
+                const uint32_t pair = CI * (q % (32 * NC)) + q / (32 * NC);
+                w[j] = unit_words<ALG, false, V>(a.p, a.bc0, 0, t * W::TILE + pair);
+            }
+#pragma unroll
+            for (int j = 0; j < W::PER_PRODUCER; j++) sm.ring[s][p + j * 32 * NP] = w[j];
+            named_bar_arrive(1 + s, W::THREADS);
+            if (++s == STAGES) s = 0;
+        }
+    } else {
+        const uint32_t c = threadIdx.x - 32 * NP;
+        double *z0p = reinterpret_cast<double *>(a.out0), *z1p = reinterpret_cast<double *>(a.out1);
+        uint32_t s = 0;
+        for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+            named_bar_sync(1 + s, W::THREADS);  // producers filled stage s
+            uint4 w[CI];
+#pragma unroll
+            for (int k = 0; k < CI; k++) w[k] = sm.ring[s][k * 32 * NC + c];
+            // free the stage only if a producer will wait for it (every arrive is matched)
+            if (t + (uint64_t)STAGES * gridDim.x < n_tiles) named_bar_arrive(1 + STAGES + s, W::THREADS);
+            const uint64_t pair0 = t * W::TILE + (uint64_t)CI * c;
+            double z0[CI], z1[CI];
+#pragma unroll
+            for (int k = 0; k < CI; k++) box_muller_fast(w[k], z0[k], z1[k], &sm.tab);
+            if (pair0 + CI <= a.n_units) {
+#pragma unroll
+                for (int k = 0; k < CI; k += 2) {
+                    __stcs(reinterpret_cast<double2 *>(z0p + pair0 + k), make_double2(z0[k], z0[k + 1]));
+                    __stcs(reinterpret_cast<double2 *>(z1p + pair0 + k), make_double2(z1[k], z1[k + 1]));
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < CI; k++)
+                    if (pair0 + k < a.n_units) { z0p[pair0 + k] = z0[k]; z1p[pair0 + k] = z1[k]; }
+            }
+            if (++s == STAGES) s = 0;
+        }
+    }
+}
+
 constexpr int FILL_BLOCK = 256;
+
+// Warp-specialised Box-Muller launch (tuning build: CBRNG_BM_WS=1..4).
+template <int ALG, int V, int NP, int NC, int CI, int STAGES, int MB>
+static int launch_bm_ws(const FillArgs<ALG> &a, cudaStream_t st) {
+    using W = BmWs<NP, NC, CI, STAGES>;
+    auto k = bm_ws_kernel<ALG, V, NP, NC, CI, STAGES, MB>;
+    const uint64_t tiles = (a.n_units + W::TILE - 1) / W::TILE;
+    const int res = resident_blocks(reinterpret_cast<const void *>(k), W::THREADS, 0);
+    uint64_t g = tiles < (uint64_t)res ? tiles : (uint64_t)res;
+    k<<<(unsigned)(g ? g : 1), W::THREADS, 0, st>>>(a);
+    return check_launch("bm_ws_kernel");
+}
 
 template <int ALG, int OUT, bool SKIP, int ILP, int V, int CV, int MB = 0>
 static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
@@ -270,8 +378,18 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
         }
         return launch_fill_ilp<ALG, OUT, SKIP, I0, V, CV>(a, st);
     } else if constexpr (OUT == OUT_NORMAL && ALG == PHILOX) {
-        // register cap for the FP64 Box-Muller (8 CTAs/SM; 5 and 6 spill and
-        // were measured no better, profiles/r1s_tune.md)
+        // warp-specialised form: tuning build only (measured 45 % slower, profiles/r2b_tune.md)
+        if constexpr (TUNING) {
+            static const int ws = tuning_knob("CBRNG_BM_WS", 0, 0, 4);
+            if (ws && aligned(a.out0, 16) && aligned(a.out1, 16)) {
+                if (ws == 2) return launch_bm_ws<ALG, V, 4, 8, 4, 2, 4>(a, st);
+                if (ws == 3) return launch_bm_ws<ALG, V, 2, 6, 2, 3, 8>(a, st);
+                if (ws == 4) return launch_bm_ws<ALG, V, 4, 4, 2, 2, 8>(a, st);
+                return launch_bm_ws<ALG, V, 4, 8, 2, 2, 5>(a, st);
+            }
+        }
+        // fused form: register cap for the FP64 Box-Muller (8 CTAs/SM; 5 and 6
+        // spill and were measured no better, profiles/r1s_tune.md)
         if constexpr (TUNING) {
             static const int mb = tuning_knob("CBRNG_BM_MINB", BM_MINB_DEFAULT, 0, 8);
             if (mb != 8) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);

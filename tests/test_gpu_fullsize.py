@@ -90,7 +90,8 @@ def test_cfg4_every_word_matches_reference(cb, g2):
 def test_cfg3_every_value_within_tolerance(cb, oracle):
     """All 2^33 pairs of the long-stream layout (pair i: stream (42, i div 2^32),
     block i mod 2^32), compared on the host against the reference formula in
-    chunks of 2^28 pairs. Bound: 4 ulp(max(|z|, 1)) per value."""
+    chunks of 2^28 pairs. Bounds: 4 ulp(max(|z|, 1)) and 8 ulps of z per value
+    (round 2 measured: 3 and 5)."""
     import torch
     from paper_2310_19925_b200 import sharding
 
@@ -113,6 +114,7 @@ def test_cfg3_every_value_within_tolerance(cb, oracle):
     torch.cuda.empty_cache()
     print("configs[3] 2^34 values:", json.dumps(worst))
     assert worst["over_tol"] == 0 and worst["max_units"] <= 4.0, worst
+    assert worst["max_rel_ulps"] <= 8.0, worst  # relative error bound, ulps of z
 
 
 def test_cfg2_full_walk_1024_pids(cb, oracle):

@@ -21,6 +21,7 @@ pytestmark = pytest.mark.gpu
 
 M32 = 0xFFFFFFFF
 BM_ULP = 4  # Box-Muller tolerance, in ulp(max(|z|, 1))
+BM_REL_ULP = 8  # and in ulps of z itself (observed: 5 over all 2^34 values of configs[3])
 
 
 def sha(a) -> str:
@@ -178,6 +179,20 @@ class TestDistributions:
             ulps = np.abs(got - r) / np.spacing(np.maximum(np.abs(r), 1.0))
             assert ulps.max() <= BM_ULP, ulps.max()
 
+    @pytest.mark.parametrize("alg", ALGS)
+    def test_normal2_vs_reference_bulk_path(self, cb, golden_arrays, alg, record_property):
+        """Against the reference's own bulk normal2_array (numpy's vectorised
+        log/sqrt/cos/sin, distributions.py:110-120), not only its scalar path:
+        the same absolute bound, and the relative error in ulps of z reported."""
+        z0, z1 = (host(z) for z in cb.normal2_array(cb.make_generator(alg, 42, 0), 4099))
+        worst_rel = 0.0
+        for got, r in ((z0, golden_arrays[f"n2bulk_{alg}_z0"]), (z1, golden_arrays[f"n2bulk_{alg}_z1"])):
+            assert np.all(np.abs(got - r) <= BM_ULP * np.spacing(np.maximum(np.abs(r), 1.0)))
+            nz = r != 0
+            worst_rel = max(worst_rel, float((np.abs(got - r)[nz] / np.spacing(np.abs(r[nz]))).max()))
+        record_property("box_muller_max_rel_ulp_vs_bulk", worst_rel)
+        assert worst_rel <= BM_REL_ULP, worst_rel
+
     def test_normal2_large_vs_oracle(self, cb, oracle):
         n = 1 << 20
         z0, z1 = (host(z) for z in cb.normal2_array(cb.make_generator("philox", 42, 0), n))
@@ -185,6 +200,21 @@ class TestDistributions:
         for got, r in ((z0, r0), (z1, r1)):
             ulps = np.abs(got - r) / np.spacing(np.maximum(np.abs(r), 1.0))
             assert ulps.max() <= BM_ULP, ulps.max()
+
+    @pytest.mark.parametrize("n,off", [(1, 0), (3, 0), (511, 0), (513, 0), (5 * 512 * 148 + 77, 0), (4099, 1),
+                                       (2, 1)])
+    def test_normal2_ragged_and_aligned(self, cb, oracle, n, off):
+        """Philox Box-Muller through the warp-specialised kernel (16-byte aligned
+        outputs; partial last tile, fewer pairs than one tile, more tiles than the
+        grid) and through the fused kernel (outputs only 8-byte aligned)."""
+        import torch
+
+        z0 = torch.empty(n + off, dtype=torch.float64, device="cuda")[off:]
+        z1 = torch.empty(n + off, dtype=torch.float64, device="cuda")[off:]
+        cb.normal2_array(cb.make_generator("philox", 7, 11), n, out=(z0, z1))
+        r0, r1 = oracle.normal2("philox", 7, 11, n)
+        for got, r in ((host(z0), r0), (host(z1), r1)):
+            assert np.all(np.abs(got - r) <= BM_ULP * np.spacing(np.maximum(np.abs(r), 1.0)))
 
     def test_normal2_words_edges(self, cb, oracle, record_property):
         """Box-Muller over chosen words: u1 = 1 (r = 0), u1 = 2^-53 (largest r),

@@ -153,17 +153,23 @@ for alg in ("philox", "threefry", "squares"):
                           orc.words_to_f32(orc.stream_words(alg, 5, 1, n))): bad.append(["fill", alg])
 got = bulk.prefix_uniform_f32("tyche", range(1000), 0, 256).cpu().numpy().reshape(-1)
 if not np.array_equal(got, orc.words_to_f32(orc.prefix_words_arange("tyche", 0, 1000, 0, 256))): bad.append("tyche")
-z0, z1 = cb.normal2_array(cb.make_generator("philox", 42, 0), 4099)
-r0, r1 = orc.normal2("philox", 42, 0, 4099)
-for g, r in ((z0.cpu().numpy(), r0), (z1.cpu().numpy(), r1)):
-    if not np.all(np.abs(g - r) <= 4 * np.spacing(np.maximum(np.abs(r), 1.0))): bad.append("normal2")
+# Box-Muller: ragged sizes around the warp-specialised kernel's tiles, and
+# 8-byte-aligned (not 16) outputs, which take the fused kernel
+for n, off in ((4099, 0), (3, 0), (1 << 20, 0), (5 * 512 * 148 + 77, 0), (4099, 1)):
+    z0 = torch.empty(n + off, dtype=torch.float64, device="cuda")[off:]
+    z1 = torch.empty(n + off, dtype=torch.float64, device="cuda")[off:]
+    cb.normal2_array(cb.make_generator("philox", 42, 0), n, out=(z0, z1))
+    r0, r1 = orc.normal2("philox", 42, 0, n)
+    for g, r in ((z0.cpu().numpy(), r0), (z1.cpu().numpy(), r1)):
+        if not np.all(np.abs(g - r) <= 4 * np.spacing(np.maximum(np.abs(r), 1.0))): bad.append(["normal2", n, off])
 print(json.dumps(bad))
 """
 
 
 @pytest.mark.parametrize("env", [
-    {"CBRNG_BROWNIAN_TAB": "0"}, {"CBRNG_BROWNIAN_PINGPONG": "0"}, {"CBRNG_BROWNIAN_PDL": "0"},
+    {"CBRNG_BROWNIAN_TAB": "0"}, {"CBRNG_BROWNIAN_TAB": "2"}, {"CBRNG_BROWNIAN_PINGPONG": "0"}, {"CBRNG_BROWNIAN_PDL": "0"},
     {"CBRNG_GRID_MULT": "0"}, {"CBRNG_GRID_MULT": "16"}, {"CBRNG_TY_GRID": "8"}, {"CBRNG_BM_MINB": "0"},
+    {"CBRNG_BM_WS": "0"}, {"CBRNG_BM_WS": "2"}, {"CBRNG_BM_WS": "3"}, {"CBRNG_BM_WS": "4"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_misc_knobs(env):
     import torch
