@@ -46,6 +46,25 @@ __host__ __device__ __forceinline__ void mulhilo(uint32_t a, uint32_t b, uint32_
     lo = (uint32_t)p;
 }
 
+// The Philox multipliers in the constant bank: an IMAD can read one directly.
+static __constant__ uint32_t c_philox_m[2] = {0xD2511F53u, 0xCD9E8D57u};
+
+// M * b as separate high (IMAD.HI, immediate M) and low (IMAD, constant-bank M,
+// so ptxas cannot fuse the pair back into one IMAD.WIDE) halves. In kernels
+// that mix the cipher with FP64 work the split form overlaps with DFMA/DMUL,
+// while IMAD.WIDE and the FP64 ops all but serialise on B200 (pipe probes,
+// profiles/r2f_probe_pipes.json: IMAD.WIDE + 2 DFMA 7.8 cycles per warp and
+// set, IMAD.HI + IMAD + 2 DFMA 6.6, for 4 and 6 heavy-pipe cycles alone).
+template <uint32_t M, bool SPLIT>
+__device__ __forceinline__ void mulhilo_c(uint32_t b, uint32_t &hi, uint32_t &lo) {
+    if constexpr (SPLIT) {
+        hi = __umulhi(b, M);
+        lo = b * c_philox_m[M == 0xD2511F53u ? 0 : 1];
+    } else {
+        mulhilo(M, b, hi, lo);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Philox4x32-10 (generators.py:101-122)
 // ---------------------------------------------------------------------------
@@ -112,31 +131,45 @@ __host__ __device__ inline PhiloxStream philox_stream_setup(uint64_t seed, uint3
     return p;
 }
 
+template <bool SPLIT>
+__device__ __forceinline__ void philox_round_d(uint32_t &c0, uint32_t &c1, uint32_t &c2, uint32_t &c3, uint32_t k0,
+                                               uint32_t k1) {
+    uint32_t h0, l0, h1, l1;
+    mulhilo_c<PHILOX_M0, SPLIT>(c0, h0, l0);
+    mulhilo_c<PHILOX_M1, SPLIT>(c2, h1, l1);
+    c0 = h1 ^ c1 ^ k0;
+    c1 = l1;
+    c2 = h0 ^ c3 ^ k1;
+    c3 = l0;
+}
+
+// SPLIT: mulhilo as IMAD.HI + IMAD (mulhilo_c), for kernels that mix in FP64.
+template <bool SPLIT = false>
 __device__ __forceinline__ uint4 philox_stream_block(const PhiloxStream& p, uint32_t bc) {
     uint32_t c0, c1, c2, c3, h, l;
     // round 0
     c0 = bc ^ p.k0_0;
     // round 1
-    mulhilo(PHILOX_M0, c0, h, l);
+    mulhilo_c<PHILOX_M0, SPLIT>(c0, h, l);
     c2 = h ^ p.a1;
     c3 = l;
     // round 2
-    mulhilo(PHILOX_M1, c2, h, l);
+    mulhilo_c<PHILOX_M1, SPLIT>(c2, h, l);
     c0 = h ^ p.b2;
     c1 = l;
     c2 = c3 ^ p.c2;
     // round 3 (c3 of round 2 is uniform and folded into e3)
     {
         uint32_t h0, l0, h1, l1;
-        mulhilo(PHILOX_M0, c0, h0, l0);
-        mulhilo(PHILOX_M1, c2, h1, l1);
+        mulhilo_c<PHILOX_M0, SPLIT>(c0, h0, l0);
+        mulhilo_c<PHILOX_M1, SPLIT>(c2, h1, l1);
         c0 = h1 ^ c1 ^ p.k0_3;
         c1 = l1;
         c2 = h0 ^ p.e3;
         c3 = l0;
     }
 #pragma unroll
-    for (int r = 0; r < 6; r++) philox_round(c0, c1, c2, c3, p.rk0[r], p.rk1[r]);
+    for (int r = 0; r < 6; r++) philox_round_d<SPLIT>(c0, c1, c2, c3, p.rk0[r], p.rk1[r]);
     return make_uint4(c0, c1, c2, c3);
 }
 
@@ -518,6 +551,7 @@ struct SquaresStream {
     uint64_t key;
     uint64_t base;  // (sc << 32) * key mod 2^64
     uint64_t k2x2;  // 2 key^2 (squares_x4_inc)
+    uint64_t k2x4;  // 4 key^2
     uint64_t ebase; // ((sc << 33) + 1) key^2 + key: E for counter 0
 };
 
@@ -527,6 +561,7 @@ inline SquaresStream squares_stream_setup(uint64_t seed, uint32_t sc) {
     p.base = ((uint64_t)sc << 32) * p.key;
     const uint64_t k2 = p.key * p.key;
     p.k2x2 = 2 * k2;
+    p.k2x4 = 4 * k2;
     p.ebase = (((uint64_t)sc << 33) + 1) * k2 + p.key;
     return p;
 }
@@ -549,18 +584,48 @@ __device__ __forceinline__ uint32_t squares_rounds_234(uint64_t r, uint64_t y, u
     return (uint32_t)(p >> 32) + t + t;
 }
 
+// An opaque zero in the constant bank: ptxas cannot fold it, and IADD3 takes
+// it as a c[] operand (no register).
+static __constant__ uint32_t c_zero = 0;
+
+// 64-bit a + b whose high half is a 3-input add against an opaque zero
+// (c_zero): ptxas then emits IADD3.X on the ALU pipe. Left as a
+// 2-input addc it picks IMAD.X for about half of them, a slot on the
+// FMA-heavy pipe that bounds Squares (1.1 of its 12.1 slots per word, r2d).
+__device__ __forceinline__ uint64_t add64_alu(uint64_t a, uint64_t b) {
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;\n\tadd.u32 %1, %1, %6;"
+        : "=r"(lo), "=r"(hi)
+        : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)), "r"(c_zero));
+    return ((uint64_t)hi << 32) | lo;
+}
+
+// 64-bit a + b + c: one IADD3 (two carries out) and one IADD3.X, both ALU.
+__device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) {
+    uint32_t lo, hi;
+    asm("{.reg .u32 t0, t1;\n\tadd.cc.u32 t0, %2, %4;\n\taddc.u32 t1, %3, %5;\n\t"
+        "add.cc.u32 %0, t0, %6;\n\taddc.u32 %1, t1, %7;}"
+        : "=r"(lo), "=r"(hi)
+        : "r"((uint32_t)a), "r"((uint32_t)(a >> 32)), "r"((uint32_t)b), "r"((uint32_t)(b >> 32)),
+          "r"((uint32_t)c), "r"((uint32_t)(c >> 32)));
+    return ((uint64_t)hi << 32) | lo;
+}
+
 // Four consecutive counters with round 1 stepped by finite differences: for
 // x_k = x_0 + k key, r_k = x_k^2 + x_k satisfies r_{k+1} = r_k + E_k with
 // E_k = 2 key x_k + key^2 + key and E_{k+1} = E_k + 2 key^2 (all mod 2^64), so
 // three of the four round-1 squarings (an IMAD.WIDE + IMAD each on the
 // FMA-heavy pipe, which bounds Squares) become 64-bit adds on the ALU pipe.
-// z_k = x_k + key = x_{k+1}.
-__device__ __forceinline__ uint4 squares_x4_inc(uint64_t x0, uint64_t e0, uint64_t key, uint64_t k2x2) {
-    const uint64_t x1 = add64_opaque(x0, key), x2 = add64_opaque(x1, key), x3 = add64_opaque(x2, key);
-    const uint64_t x4 = add64_opaque(x3, key);
-    const uint64_t e1 = add64_opaque(e0, k2x2), e2 = add64_opaque(e1, k2x2);
+// E_1, E_2 are folded into 3-input adds, r_2 = r_1 + E_0 + 2 key^2 and
+// r_3 = r_2 + E_0 + 4 key^2, which ptxas cannot put on IMAD.X.
+// z_k = x_k + key = x_{k+1}. k2x2 = 2 key^2, k2x4 = 4 key^2.
+__device__ __forceinline__ uint4 squares_x4_inc(uint64_t x0, uint64_t e0, uint64_t key, uint64_t k2x2, uint64_t k2x4,
+                                                uint64_t *x4_out = nullptr) {
+    const uint64_t x1 = add64_alu(x0, key), x2 = add64_alu(x1, key), x3 = add64_alu(x2, key);
+    const uint64_t x4 = add64_alu(x3, key);
+    if (x4_out) *x4_out = x4;
     const uint64_t r0 = squares_r1(x0);
-    const uint64_t r1 = add64_opaque(r0, e0), r2 = add64_opaque(r1, e1), r3 = add64_opaque(r2, e2);
+    const uint64_t r1 = add64_alu(r0, e0), r2 = add64_3(r1, e0, k2x2), r3 = add64_3(r2, e0, k2x4);
     return make_uint4(squares_rounds_234(r0, x0, x1), squares_rounds_234(r1, x1, x2), squares_rounds_234(r2, x2, x3),
                       squares_rounds_234(r3, x3, x4));
 }

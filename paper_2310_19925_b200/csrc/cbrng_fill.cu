@@ -38,9 +38,10 @@ struct FillArgs {
 };
 
 // CV: where the f32 map's shift / convert / scale run (u32_to_f32_cv).
-template <int OUT, int CV = 0>
+// BV: the lane's view of the Box-Muller tables (OUT_NORMAL only).
+template <int OUT, int CV = 0, class BV = BmView<>>
 __device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0,
-                                           const BmTables *bm_tab = nullptr) {
+                                           const BV &bm = BV{}) {
     if constexpr (OUT == OUT_U32) {
         __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
     } else if constexpr (OUT == OUT_F32) {
@@ -49,7 +50,7 @@ __device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, u
         __stcs(reinterpret_cast<double2 *>(out0) + u, make_double2(u32x2_to_f64(w.x, w.y), u32x2_to_f64(w.z, w.w)));
     } else {
         double z0, z1;
-        box_muller_fast(w, z0, z1, bm_tab);
+        box_muller_fast(w, z0, z1, bm);
         __stcs(reinterpret_cast<double *>(out0) + u, z0);
         __stcs(reinterpret_cast<double *>(out1) + u, z1);
     }
@@ -70,14 +71,37 @@ __device__ __forceinline__ void store_tail(void *out0, uint64_t u, uint32_t tail
 
 // One fill job, warp-strided: warp `warp` of `nwarps` takes tiles warp,
 // warp + nwarps, ...; the last warp also writes the remainder and the tail.
-template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV>
+// PIPE (Box-Muller): software-pipelined tiles, the cipher blocks of the warp's
+// next tile are generated in the same loop body as the current tile's FP64
+// transform, so one warp's instruction stream mixes FMA-heavy (IMAD.WIDE) and
+// FP64 work instead of alternating between a cipher phase and a transform phase.
+template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV, class BV = BmView<>, bool PIPE = false>
 __device__ __forceinline__ void fill_job(const FillArgs<ALG> &a, uint64_t warp, uint64_t nwarps, uint32_t lane,
-                                         const BmTables *bmt) {
+                                         const BV &bmt = BV{}) {
     constexpr uint32_t TILE = 32 * ILP;
     // Full warp tiles: no bounds checks, all ILP cipher evaluations issued
     // before the stores.
     const uint64_t n_full = a.n_units / TILE;
-    for (uint64_t t = warp; t < n_full; t += nwarps) {
+    if constexpr (PIPE) {
+        uint4 wn[ILP];
+        if (warp < n_full) {
+#pragma unroll
+            for (int j = 0; j < ILP; j++) wn[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, warp * TILE + lane + 32 * j);
+        }
+        for (uint64_t t = warp; t < n_full; t += nwarps) {
+            uint4 w[ILP];
+#pragma unroll
+            for (int j = 0; j < ILP; j++) w[j] = wn[j];
+            // the next tile (the last iteration recomputes its own: a select, not a branch)
+            const uint64_t tn = t + nwarps < n_full ? t + nwarps : t;
+#pragma unroll
+            for (int j = 0; j < ILP; j++) wn[j] = unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, tn * TILE + lane + 32 * j);
+#pragma unroll
+            for (int j = 0; j < ILP; j++)
+                store_unit<OUT, CV, BV>(a.out0, a.out1, t * TILE + lane + 32 * j, w[j], a.m24, bmt);
+        }
+    }
+    for (uint64_t t = PIPE ? n_full : warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
         if constexpr (ALG == SQUARES && V == 2) {
@@ -89,9 +113,9 @@ __device__ __forceinline__ void fill_job(const FillArgs<ALG> &a, uint64_t warp, 
             const uint64_t sx = a.p.key << 7, se = a.p.k2x2 << 7;
 #pragma unroll
             for (int j = 0; j < ILP; j++) {
-                w[j] = squares_x4_inc(x, e, a.p.key, a.p.k2x2);
-                x = add64_opaque(x, sx);
-                e = add64_opaque(e, se);
+                w[j] = squares_x4_inc(x, e, a.p.key, a.p.k2x2, a.p.k2x4);
+                x = add64_alu(x, sx);
+                e = add64_alu(e, se);
             }
         } else if constexpr (ALG == SQUARES && V == 1) {
             // no counter wrap anywhere in the fill: unit u's first product
@@ -110,12 +134,12 @@ __device__ __forceinline__ void fill_job(const FillArgs<ALG> &a, uint64_t warp, 
         }
 #pragma unroll
         for (int j = 0; j < ILP; j++)
-            store_unit<OUT, CV>(a.out0, a.out1, base + 32 * j, w[j], a.m24, bmt);
+            store_unit<OUT, CV, BV>(a.out0, a.out1, base + 32 * j, w[j], a.m24, bmt);
     }
     // Remainder (< one tile) and the partial trailing unit: the last warp of the grid.
     if (warp == nwarps - 1) {
         for (uint64_t u = n_full * TILE + lane; u < a.n_units; u += 32)
-            store_unit<OUT>(a.out0, a.out1, u, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, u), 0, bmt);
+            store_unit<OUT, 0, BV>(a.out0, a.out1, u, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, u), 0, bmt);
         if (a.tail && lane == 0)
             store_tail<OUT>(a.out0, a.n_units, a.tail, unit_words<ALG, SKIP, V>(a.p, a.bc0, a.skip, a.n_units));
     }
@@ -124,17 +148,24 @@ __device__ __forceinline__ void fill_job(const FillArgs<ALG> &a, uint64_t warp, 
 // MB: minimum resident CTAs per SM for the register allocator (0 = unconstrained).
 template <int ALG, int OUT, int ILP, bool SKIP, int V, int CV, int MB = 0>
 __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
+    static_assert(OUT != OUT_NORMAL, "normal_fill_kernel");
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    // Box-Muller's log table, staged once per CTA (cbrng_bm.cuh)
-    __shared__ std::conditional_t<OUT == OUT_NORMAL, BmTables, char> s_bm;
-    const BmTables *bmt = nullptr;
-    if constexpr (OUT == OUT_NORMAL) {
-        bm_stage_table(&s_bm);
-        bmt = &s_bm;
-    }
-    fill_job<ALG, OUT, ILP, SKIP, V, CV>(a, warp, nwarps, lane, bmt);
+    fill_job<ALG, OUT, ILP, SKIP, V, CV>(a, warp, nwarps, lane);
+}
+
+// Box-Muller fill: NT threads per CTA, LC / SC interleaved copies of the log /
+// sincos tables in shared memory (cbrng_bm.cuh), MB CTAs per SM for the
+// register allocator.
+template <int ALG, int ILP, bool SKIP, int V, int LC, int SC, int NT, int MB, bool PIPE = false>
+__global__ void __launch_bounds__(NT, MB) normal_fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    const BmView<LC, SC> v = bm_stage_table(reinterpret_cast<BmTables<LC, SC> *>(s_dyn));
+    fill_job<ALG, OUT_NORMAL, ILP, SKIP, V, 0, BmView<LC, SC>, PIPE>(a, warp, nwarps, lane, v);
 }
 
 // Several counter-based fills in one launch (cbrng_words_multi /
@@ -174,8 +205,9 @@ __global__ void __launch_bounds__(256, MB) multi_fill_kernel(const __grid_consta
 // one thread walks the chain. Latency-bound (~12 dependent ALU ops per word).
 template <int OUT>
 __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1, uint32_t *state_out, uint32_t z) {
-    __shared__ std::conditional_t<OUT == OUT_NORMAL, BmTables, char> s_bm;
-    if constexpr (OUT == OUT_NORMAL) bm_stage_table(&s_bm);
+    __shared__ std::conditional_t<OUT == OUT_NORMAL, BmTables<>, char> s_bm;
+    BmView<> bv{};
+    if constexpr (OUT == OUT_NORMAL) bv = bm_stage_table(&s_bm);
     uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
     for (uint64_t i = 0; i < n; i++) {
         if constexpr (OUT == OUT_U32) {
@@ -196,7 +228,7 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
             tyche_mix_alu(a, b, c, d, z); w.z = b;
             tyche_mix_alu(a, b, c, d, z); w.w = b;
             double z0, z1;
-            box_muller_fast(w, z0, z1, reinterpret_cast<const BmTables *>(&s_bm));
+            box_muller_fast(w, z0, z1, bv);
             reinterpret_cast<double *>(out0)[i] = z0;
             reinterpret_cast<double *>(out1)[i] = z1;
         }
@@ -211,126 +243,18 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
 // with scripted generators, test_distributions.py:29-40, 178-186).
 __global__ void __launch_bounds__(256) normal2_words_kernel(const uint4 *__restrict__ w, uint64_t n_pairs,
                                                             double *__restrict__ z0, double *__restrict__ z1) {
-    __shared__ BmTables s_bm;
-    bm_stage_table(&s_bm);
+    __shared__ BmTables<> s_bm;
+    const BmView<> bv = bm_stage_table(&s_bm);
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pairs;
          i += (uint64_t)gridDim.x * blockDim.x) {
         double a, b;
-        box_muller_fast(w[i], a, b, &s_bm);
+        box_muller_fast(w[i], a, b, bv);
         z0[i] = a;
         z1[i] = b;
     }
 }
 
-// ---------------------------------------------------------------------------
-// Warp-specialised Box-Muller fill (single stream, block-aligned).
-//
-// The fused form (fill_kernel<.., OUT_NORMAL, ..>) runs the Philox block (16
-// IMAD.WIDE + 18 LOP3: the FMA-heavy pipe) and the transform (35 FP64 ops) in
-// the same warp, so all warps alternate between a heavy-pipe phase and an
-// FP64 phase more or less in step and neither pipe is fed steadily (ncu r2a:
-// 63 % issue, math-pipe throttle and dispatch stalls on both phases). Here NP
-// producer warps generate the 4-word blocks of a tile of pairs into a
-// shared-memory ring and NC consumer warps turn them into (z0, z1) and store
-// them, so every SM sub-partition always has warps of both kinds ready.
-// Hand-off per stage: named barriers FULL[s] (producers arrive, consumers
-// wait) and EMPTY[s] (consumers arrive, producers wait), 16 B of shared
-// memory per pair each way.
-//
-// Layout: tile = NC*32*CI pairs. Consumer thread c owns pairs CI*c .. CI*c+CI-1
-// (16-byte stores of pair-adjacent z0 / z1 doubles); pair CI*c + k sits in
-// slot k*(NC*32) + c, so producer stores and consumer loads are both
-// conflict-free 128-bit accesses.
-template <int NP, int NC, int CI, int STAGES>
-struct BmWs {
-    static constexpr int THREADS = 32 * (NP + NC);
-    static constexpr int TILE = 32 * NC * CI;        // pairs per stage
-    static constexpr int PER_PRODUCER = TILE / (32 * NP);
-    static_assert(TILE % (32 * NP) == 0, "tile must split evenly over producers");
-    static_assert(CI % 2 == 0, "consumers store pair-adjacent 16-byte vectors");
-    struct Smem {
-        BmTables tab;
-        uint4 ring[STAGES][TILE];
-    };
-};
-
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-template <int ALG, int V, int NP, int NC, int CI, int STAGES, int MB>
-__global__ void __launch_bounds__(BmWs<NP, NC, CI, STAGES>::THREADS, MB)
-    bm_ws_kernel(const __grid_constant__ FillArgs<ALG> a) {
-    using W = BmWs<NP, NC, CI, STAGES>;
-    __shared__ typename W::Smem sm;
-    bm_stage_table(&sm.tab);
-    const uint32_t warp = threadIdx.x >> 5;
-    const uint64_t n_tiles = (a.n_units + W::TILE - 1) / W::TILE;
-    // barrier ids: 1 + s = FULL[s], 1 + STAGES + s = EMPTY[s] (0 is __syncthreads)
-    if (warp < NP) {
-        const uint32_t p = threadIdx.x;
-        uint32_t s = 0;
-        for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            if (t >= (uint64_t)STAGES * gridDim.x) named_bar_sync(1 + STAGES + s, W::THREADS);  // stage s consumed
-            uint4 w[W::PER_PRODUCER];
-#pragma unroll
-            for (int j = 0; j < W::PER_PRODUCER; j++) {
-                const uint32_t q = p + j * 32 * NP;
-                const uint32_t pair = CI * (q % (32 * NC)) + q / (32 * NC);
-                w[j] = unit_words<ALG, false, V>(a.p, a.bc0, 0, t * W::TILE + pair);
-            }
-#pragma unroll
-            for (int j = 0; j < W::PER_PRODUCER; j++) sm.ring[s][p + j * 32 * NP] = w[j];
-            named_bar_arrive(1 + s, W::THREADS);
-            if (++s == STAGES) s = 0;
-        }
-    } else {
-        const uint32_t c = threadIdx.x - 32 * NP;
-        double *z0p = reinterpret_cast<double *>(a.out0), *z1p = reinterpret_cast<double *>(a.out1);
-        uint32_t s = 0;
-        for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-            named_bar_sync(1 + s, W::THREADS);  // producers filled stage s
-            uint4 w[CI];
-#pragma unroll
-            for (int k = 0; k < CI; k++) w[k] = sm.ring[s][k * 32 * NC + c];
-            // free the stage only if a producer will wait for it (every arrive is matched)
-            if (t + (uint64_t)STAGES * gridDim.x < n_tiles) named_bar_arrive(1 + STAGES + s, W::THREADS);
-            const uint64_t pair0 = t * W::TILE + (uint64_t)CI * c;
-            double z0[CI], z1[CI];
-#pragma unroll
-            for (int k = 0; k < CI; k++) box_muller_fast(w[k], z0[k], z1[k], &sm.tab);
-            if (pair0 + CI <= a.n_units) {
-#pragma unroll
-                for (int k = 0; k < CI; k += 2) {
-                    __stcs(reinterpret_cast<double2 *>(z0p + pair0 + k), make_double2(z0[k], z0[k + 1]));
-                    __stcs(reinterpret_cast<double2 *>(z1p + pair0 + k), make_double2(z1[k], z1[k + 1]));
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < CI; k++)
-                    if (pair0 + k < a.n_units) { z0p[pair0 + k] = z0[k]; z1p[pair0 + k] = z1[k]; }
-            }
-            if (++s == STAGES) s = 0;
-        }
-    }
-}
-
 constexpr int FILL_BLOCK = 256;
-
-// Warp-specialised Box-Muller launch (tuning build: CBRNG_BM_WS=1..4).
-template <int ALG, int V, int NP, int NC, int CI, int STAGES, int MB>
-static int launch_bm_ws(const FillArgs<ALG> &a, cudaStream_t st) {
-    using W = BmWs<NP, NC, CI, STAGES>;
-    auto k = bm_ws_kernel<ALG, V, NP, NC, CI, STAGES, MB>;
-    const uint64_t tiles = (a.n_units + W::TILE - 1) / W::TILE;
-    const int res = resident_blocks(reinterpret_cast<const void *>(k), W::THREADS, 0);
-    uint64_t g = tiles < (uint64_t)res ? tiles : (uint64_t)res;
-    k<<<(unsigned)(g ? g : 1), W::THREADS, 0, st>>>(a);
-    return check_launch("bm_ws_kernel");
-}
 
 template <int ALG, int OUT, bool SKIP, int ILP, int V, int CV, int MB = 0>
 static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
@@ -361,15 +285,68 @@ constexpr int fill_ilp_default() {
 // block_at) and the f32 conversion placement CV (see u32_to_f32_cv) per
 // generator. Tuning build: CBRNG_FILL_ILP=8|12|16, CBRNG_TF_VARIANT=0..8,
 // CBRNG_CVT=0..5, CBRNG_BM_MINB=0|8, CBRNG_SQ_INC=0|1, CBRNG_MULTI=0|1.
-constexpr int BM_MINB_DEFAULT = 8;  // r1s sweep: 0 -> 8 = +4 % (profiles/r1s_tune.md)
+// Box-Muller fill shape (normal_fill_kernel): ILP pairs per thread, LC / SC
+// table copies, NT threads per CTA, MB CTAs per SM (profiles/r2e_tune.md).
+constexpr int BM_ILP = 8, BM_LC = 8, BM_SC = 2, BM_NT = 1024, BM_MB = 2, BM_LAYOUT_DEFAULT = 5;
+
+template <int ALG, bool SKIP, int V, int ILP, int LC, int SC, int NT, int MB, bool PIPE = false>
+static int launch_normal(const FillArgs<ALG> &a, cudaStream_t st) {
+    auto k = normal_fill_kernel<ALG, ILP, SKIP, V, LC, SC, NT, MB, PIPE>;
+    constexpr size_t smem = sizeof(BmTables<LC, SC>);
+    // per launch: the attribute is per device and the ABI serves any current device
+    if (smem > 48 * 1024) {
+        const int rc = check_cuda(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                                  "normal_fill_kernel shared-memory attribute");
+        if (rc) return rc;
+    }
+    // persistent: one resident grid (each CTA stages smem bytes of tables once)
+    const uint64_t work = (a.n_units + (NT * ILP) - 1) / (NT * ILP);
+    uint64_t g = (uint64_t)resident_blocks(reinterpret_cast<const void *>(k), NT, smem);
+    if constexpr (TUNING) g *= (uint64_t)tuning_knob("CBRNG_BM_GRID", 1, 1, 8);
+    if (work < g) g = work;
+    k<<<(unsigned)(g ? g : 1), NT, smem, st>>>(a);
+    return check_launch("normal_fill_kernel");
+}
+
 template <int ALG> constexpr int cv_default() { return 4; }  // all three fills: SHF + I2F (XU) + FMUL
+
+// Tuning build: the Box-Muller fill shapes of CBRNG_BM_LAYOUT (profiles/r2e_tune.md).
+template <int ALG, bool SKIP, int VS>
+static int launch_normal_layout(const FillArgs<ALG> &a, cudaStream_t st, int lay) {
+    switch (lay) {
+        case 8: return launch_normal<ALG, SKIP, VS, 4, 8, 2, 512, 2, true>(a, st);
+        case 9: return launch_normal<ALG, SKIP, VS, 4, 8, 4, 1024, 1, true>(a, st);
+        case 10: return launch_normal<ALG, SKIP, VS, 2, 8, 2, 1024, 2, true>(a, st);
+        case 11: return launch_normal<ALG, SKIP, VS, 4, 8, 2, 1024, 2, true>(a, st);
+        case 12: return launch_normal<ALG, SKIP, VS, 8, 8, 2, 1024, 1>(a, st);
+        case 0: return launch_normal<ALG, SKIP, VS, 8, 1, 1, 256, 8>(a, st);
+        case 1: return launch_normal<ALG, SKIP, VS, 8, 2, 1, 256, 8>(a, st);
+        case 2: return launch_normal<ALG, SKIP, VS, 8, 8, 1, 512, 4>(a, st);
+        case 3: return launch_normal<ALG, SKIP, VS, 8, 4, 2, 512, 4>(a, st);
+        case 4: return launch_normal<ALG, SKIP, VS, 8, 8, 4, 1024, 2>(a, st);
+        case 5: return launch_normal<ALG, SKIP, VS, 8, 8, 2, 1024, 2>(a, st);
+        case 6: return launch_normal<ALG, SKIP, VS, 4, 8, 2, 1024, 2>(a, st);
+        default: return launch_normal<ALG, SKIP, VS, 8, 8, 1, 256, 0>(a, st);
+    }
+}
 
 template <int ALG, int OUT, bool SKIP, int V, int CV>
 static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
-    if constexpr (SKIP) {
+    if constexpr (SKIP && OUT == OUT_NORMAL) {
+        return launch_normal<ALG, SKIP, V, 2, 1, 1, 256, 0>(a, st);  // resumed mid-block: rare, 2 blocks per unit
+    } else if constexpr (SKIP) {
         return launch_fill_ilp<ALG, OUT, SKIP, 2, V, CV>(a, st);  // resumed mid-block: rare, 2 blocks per unit
     } else if constexpr (OUT == OUT_U32 || OUT == OUT_F32) {
         constexpr int I0 = fill_ilp_default<ALG, OUT>();
+        if constexpr (TUNING && ALG == SQUARES) {
+            // register cap: 6 CTAs/SM (<= 40 registers) instead of 5 at 48
+            static const int mb = tuning_knob("CBRNG_SQ_MINB", 0, 0, 8);
+            if (mb == 6) {
+                static const int ilp = tuning_knob("CBRNG_FILL_ILP", I0, 8, 16);
+                if (ilp == 12) return launch_fill_ilp<ALG, OUT, SKIP, 12, V, CV, 6>(a, st);
+                return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV, 6>(a, st);
+            }
+        }
         if constexpr (TUNING) {
             static const int ilp = tuning_knob("CBRNG_FILL_ILP", I0, 8, 16);
             if (ilp == 16) return launch_fill_ilp<ALG, OUT, SKIP, 16, V, CV>(a, st);
@@ -377,24 +354,15 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
             return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
         }
         return launch_fill_ilp<ALG, OUT, SKIP, I0, V, CV>(a, st);
-    } else if constexpr (OUT == OUT_NORMAL && ALG == PHILOX) {
-        // warp-specialised form: tuning build only (measured 45 % slower, profiles/r2b_tune.md)
-        if constexpr (TUNING) {
-            static const int ws = tuning_knob("CBRNG_BM_WS", 0, 0, 4);
-            if (ws && aligned(a.out0, 16) && aligned(a.out1, 16)) {
-                if (ws == 2) return launch_bm_ws<ALG, V, 4, 8, 4, 2, 4>(a, st);
-                if (ws == 3) return launch_bm_ws<ALG, V, 2, 6, 2, 3, 8>(a, st);
-                if (ws == 4) return launch_bm_ws<ALG, V, 4, 4, 2, 2, 8>(a, st);
-                return launch_bm_ws<ALG, V, 4, 8, 2, 2, 5>(a, st);
-            }
+    } else if constexpr (OUT == OUT_NORMAL) {
+        if constexpr (TUNING && ALG == PHILOX && !SKIP) {
+            // CBRNG_BM_SPLIT=1: Philox mulhilo as IMAD.HI + IMAD (V 1), measured 10 % slower (r2g)
+            static const int split = tuning_knob("CBRNG_BM_SPLIT", 0, 0, 1);
+            static const int lay = tuning_knob("CBRNG_BM_LAYOUT", BM_LAYOUT_DEFAULT, 0, 12);
+            return split ? launch_normal_layout<ALG, SKIP, 1>(a, st, lay) : launch_normal_layout<ALG, SKIP, V>(a, st, lay);
         }
-        // fused form: register cap for the FP64 Box-Muller (8 CTAs/SM; 5 and 6
-        // spill and were measured no better, profiles/r1s_tune.md)
-        if constexpr (TUNING) {
-            static const int mb = tuning_knob("CBRNG_BM_MINB", BM_MINB_DEFAULT, 0, 8);
-            if (mb != 8) return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
-        }
-        return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV, BM_MINB_DEFAULT>(a, st);
+        if constexpr (ALG != PHILOX) return launch_normal<ALG, SKIP, V, 4, 8, 2, 512, 0>(a, st);  // wider cipher state
+        return launch_normal<ALG, SKIP, V, BM_ILP, BM_LC, BM_SC, BM_NT, BM_MB>(a, st);
     } else {
         return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
     }

@@ -134,18 +134,18 @@ template <> struct RowGen<SQUARES> {
     // x = ctr * key and E = 2 key x + key^2 + key for the row's next counter,
     // stepped by 4 counters per call (64-bit adds; rows never wrap the 32-bit
     // counter); round 1 of the 4 words by finite differences (squares_x4_inc)
-    uint64_t key, k2x2, x, e;
+    uint64_t key, k2x2, k2x4, x, e;
     __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) {
         key = squares_key(seed);
         const uint64_t k2 = key * key;
         k2x2 = 2 * k2;
+        k2x4 = 4 * k2;
         x = ((uint64_t)c << 32) * key;
         e = (((uint64_t)c << 33) + 1) * k2 + key;
     }
     __device__ __forceinline__ uint4 next4() {
-        const uint4 w = squares_x4_inc(x, e, key, k2x2);
-        x = add64_opaque(x, key << 2);
-        e = add64_opaque(e, k2x2 << 2);
+        const uint4 w = squares_x4_inc(x, e, key, k2x2, k2x4, &x);  // x <- x_4, the next call's x_0
+        e = add64_alu(e, k2x4 << 1);                                  // E_4 = E_0 + 8 key^2
         return w;
     }
 };

@@ -86,6 +86,12 @@ def test_ilp_variants(ilp):
     assert _run({"CBRNG_FILL_ILP": str(ilp)}) == []
 
 
+@pytest.mark.parametrize("ilp", [12, 16])
+def test_squares_register_cap(ilp):
+    """Squares fills capped at 6 CTAs/SM (<= 40 registers)."""
+    assert _run({"CBRNG_SQ_MINB": "6", "CBRNG_FILL_ILP": str(ilp)}) == []
+
+
 @pytest.mark.parametrize("ch", [4, 8])
 def test_tyche_staging_width(ch):
     assert _run({"CBRNG_TY_CH": str(ch)}) == []
@@ -168,8 +174,8 @@ print(json.dumps(bad))
 
 @pytest.mark.parametrize("env", [
     {"CBRNG_BROWNIAN_TAB": "0"}, {"CBRNG_BROWNIAN_TAB": "2"}, {"CBRNG_BROWNIAN_PINGPONG": "0"}, {"CBRNG_BROWNIAN_PDL": "0"},
-    {"CBRNG_GRID_MULT": "0"}, {"CBRNG_GRID_MULT": "16"}, {"CBRNG_TY_GRID": "8"}, {"CBRNG_BM_MINB": "0"},
-    {"CBRNG_BM_WS": "0"}, {"CBRNG_BM_WS": "2"}, {"CBRNG_BM_WS": "3"}, {"CBRNG_BM_WS": "4"},
+    {"CBRNG_GRID_MULT": "0"}, {"CBRNG_GRID_MULT": "16"}, {"CBRNG_TY_GRID": "8"}, {"CBRNG_BM_GRID": "4"},
+    *({"CBRNG_BM_LAYOUT": str(k)} for k in range(13)), {"CBRNG_BM_SPLIT": "1"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_misc_knobs(env):
     import torch

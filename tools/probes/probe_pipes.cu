@@ -128,8 +128,62 @@ __global__ void k_wide_noadd(uint64_t *out, uint32_t a) {
     if (s == 12345) out[0] = s;
 }
 
+
+// Mixes (r2f): per chain and iteration NW mul.wide.u32 (IMAD.WIDE, no addend),
+// NL lop3 (ALU) and ND DFMA with register operands, round-robin in program order
+// (asm volatile): which combinations of the Box-Muller fill's pipes co-issue.
+template <int NW, int NL, int ND>
+__global__ void k_ratio(double *out, const double *ab, uint32_t ia, uint32_t ib) {
+    const double a = ab[threadIdx.x & 1], b = ab[2 + (threadIdx.x & 1)];
+    double x[CH / 2];
+    uint32_t y[CH / 2], z[CH / 2];
+    for (int c = 0; c < CH / 2; c++) { x[c] = threadIdx.x * 1e-9 + c; y[c] = threadIdx.x * 3 + c; z[c] = c; }
+    for (int i = 0; i < IT; i++)
+#pragma unroll
+        for (int c = 0; c < CH / 2; c++) {
+#pragma unroll
+            for (int k = 0; k < (NW > NL ? (NW > ND ? NW : ND) : (NL > ND ? NL : ND)); k++) {
+                if (k < NW) { uint64_t p; asm volatile("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(y[c]), "r"(ia)); y[c] = (uint32_t)(p >> 32); z[c] ^= (uint32_t)p; }
+                if (k < NL) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(z[c]) : "r"(ia), "r"(ib));
+                if (k < ND) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(a), "d"(b));
+            }
+        }
+    double s = 0;
+    for (int c = 0; c < CH / 2; c++) s += x[c] + y[c] + z[c];
+    if (s == 1.2345) out[0] = s;
+}
+
+// r2f op-mix probe: per chain-iteration NW IMAD.WIDE (hi feeds the chain, lo
+// xor-folded), NH IMAD.HI, NI IMAD, NL LOP3, ND DFMA (register operands), NU
+// DFMA (uniform operands); asm volatile keeps the program order round-robin.
+template <int NW, int NH, int NI, int NL, int ND, int NU>
+__global__ void k_ops(double *out, const double *ab, uint32_t ia, uint32_t ib, double ua, double ub) {
+    const double a = ab[threadIdx.x & 1], b = ab[2 + (threadIdx.x & 1)];
+    constexpr int M0 = NW > NH ? NW : NH, M1 = NI > NL ? NI : NL, M2 = ND > NU ? ND : NU;
+    constexpr int MX = M0 > M1 ? (M0 > M2 ? M0 : M2) : (M1 > M2 ? M1 : M2);
+    double x[CH / 2], v[CH / 2];
+    uint32_t y[CH / 2], z[CH / 2], q[CH / 2];
+    for (int c = 0; c < CH / 2; c++) { x[c] = threadIdx.x * 1e-9 + c; v[c] = x[c] + 1; y[c] = threadIdx.x * 3 + c; z[c] = threadIdx.x ^ c; q[c] = 5 * threadIdx.x + c + 1; }
+    for (int i = 0; i < IT; i++)
+#pragma unroll
+        for (int c = 0; c < CH / 2; c++) {
+#pragma unroll
+            for (int k = 0; k < MX; k++) {
+                if (k < NW) { uint32_t lo, hi; asm volatile("{.reg .b64 t;\n\tmul.wide.u32 t, %2, %3;\n\tmov.b64 {%0, %1}, t;}" : "=r"(lo), "=r"(hi) : "r"(y[c]), "r"(ia)); y[c] = hi; z[c] ^= lo; }
+                if (k < NH) asm volatile("mul.hi.u32 %0, %0, %1;" : "+r"(q[c]) : "r"(ia));
+                if (k < NI) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(y[c]) : "r"(ia), "r"(ib));
+                if (k < NL) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(z[c]) : "r"(ia), "r"(ib));
+                if (k < ND) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(x[c]) : "d"(a), "d"(b));
+                if (k < NU) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(v[c]) : "d"(ua), "d"(ub));
+            }
+        }
+    double s = 0;
+    for (int c = 0; c < CH / 2; c++) s += x[c] + v[c] + y[c] + z[c] + q[c];
+    if (s == 1.2345) out[0] = s;
+}
+
 template <typename K, typename... A>
-static void run(const char *name, int per_iter_instr, K k, A... args) {
+static void run(const char *name, double per_iter_instr, K k, A... args) {
     int dev = 0, sms = 0, clk = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);  // kHz
@@ -167,6 +221,28 @@ int main() {
     run("I2F.F64.U64 (+IADD 64)", 1, k_i2f64, d, 7u);
     run("IMAD.WIDE (64-bit addend, alone)", 1, k_wide, (uint64_t *)u, 0x12345u);
     run("IMAD.WIDE (no addend, + SHF)", 2, k_wide_noadd, (uint64_t *)u, 0x12345u);
+    // k_ratio<NW, NL, ND>: thread-ops per chain-iteration = 2 NW (IMAD.WIDE + its XOR) + NL + ND, CH/2 chains
+    run("mix W1 (IMAD.WIDE + LOP3 xor)", 1, k_ratio<1, 0, 0>, d, (const double *)ab, 0x12345u, 7u);
+    run("mix D1 (DFMA reg)", 0.5, k_ratio<0, 0, 1>, d, (const double *)ab, 0x12345u, 7u);
+    run("mix W1 D1 (3 ops)", 1.5, k_ratio<1, 0, 1>, d, (const double *)ab, 0x12345u, 7u);
+    run("mix W1 D2 (4 ops)", 2, k_ratio<1, 0, 2>, d, (const double *)ab, 0x12345u, 7u);
+    run("mix W2 L2 D2 (8 ops)", 4, k_ratio<2, 2, 2>, d, (const double *)ab, 0x12345u, 7u);
+    run("mix W2 L0 D2 (6 ops)", 3, k_ratio<2, 0, 2>, d, (const double *)ab, 0x12345u, 7u);
+    run("mix W1 L2 D2 (6 ops)", 3, k_ratio<1, 2, 2>, d, (const double *)ab, 0x12345u, 7u);
+    // k_ops<NW, NH, NI, NL, ND, NU>: per_iter = (ops per chain-iteration) / 2; the true
+    // SASS mix of each loop is read back with tools/sass_pipes.py
+#define OPS(nw, nh, ni, nl, nd, nu) \
+    run("ops W" #nw " H" #nh " I" #ni " L" #nl " D" #nd " U" #nu, (nw + nh + ni + nl + nd + nu) / 2.0, \
+        k_ops<nw, nh, ni, nl, nd, nu>, d, (const double *)ab, 0x12345u, 7u, 1.0000001, 1e-9)
+    OPS(0, 1, 0, 0, 1, 0);
+    OPS(0, 1, 1, 0, 2, 0);
+    OPS(0, 0, 1, 0, 1, 0);
+    OPS(0, 0, 0, 1, 1, 0);
+    OPS(1, 0, 0, 0, 0, 1);
+    OPS(1, 0, 0, 0, 0, 2);
+    OPS(0, 1, 1, 0, 0, 2);
+    OPS(0, 0, 0, 0, 0, 1);
+    OPS(0, 1, 0, 0, 0, 0);
     cudaError_t e = cudaDeviceSynchronize();
     printf("# %s\n", cudaGetErrorString(e));
     return 0;

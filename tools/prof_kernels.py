@@ -12,7 +12,10 @@ import torch  # noqa: E402
 
 from paper_2310_19925_b200 import _lib, brownian  # noqa: E402
 
-which = set(sys.argv[1:]) or {"fill", "tyche", "normal", "prefix", "brownian"}
+args = [x for x in sys.argv[1:] if not x.startswith("--")]
+which = set(args) or {"fill", "tyche", "normal", "prefix", "brownian"}
+if "--tuning" in sys.argv:  # the tuning build (CBRNG_* knobs)
+    _lib.use_tuning_build()
 lib = _lib.lib()
 s = int(torch.cuda.current_stream().cuda_stream)
 N = 1 << 30
@@ -20,6 +23,10 @@ out = torch.empty(N, dtype=torch.float32, device="cuda")
 if "fill" in which:
     for alg in range(3):
         _lib.check(lib.cbrng_uniform_f32(alg, 42, 0, 0, None, N, out.data_ptr(), None, s))
+if "squares" in which:
+    _lib.check(lib.cbrng_uniform_f32(2, 42, 0, 0, None, N, out.data_ptr(), None, s))
+if "threefry" in which:
+    _lib.check(lib.cbrng_uniform_f32(1, 42, 0, 0, None, N, out.data_ptr(), None, s))
 if "tyche" in which:
     _lib.check(lib.cbrng_prefix_uniform_f32(3, None, 0, None, 0, 1 << 22, 256, out.data_ptr(), s))
 if "prefix" in which:

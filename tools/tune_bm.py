@@ -1,6 +1,6 @@
 """Time the Philox Box-Muller fill (configs[3] kernel) under tuning-build env sets.
 
-    TUNE_SETS="CBRNG_BM_WS=0;CBRNG_BM_WS=1" python tools/tune_bm.py
+    TUNE_SETS="CBRNG_BM_LAYOUT=0;CBRNG_BM_LAYOUT=5" python tools/tune_bm.py
 
 Each set runs in a fresh process bound to libcbrng_b200_tuning.so; 2^29 pairs
 (2 x 4 GiB of f64) per launch, CUDA events over 10 launches after a warm-up.
@@ -33,7 +33,7 @@ print(json.dumps({"ms": round(ms, 4), "gbs": round(P * 16 / ms / 1e6, 1), "gvalu
 
 
 def main():
-    sets = [s for s in os.environ.get("TUNE_SETS", "CBRNG_BM_WS=0;CBRNG_BM_WS=1").split(";") if s]
+    sets = [s for s in os.environ.get("TUNE_SETS", "CBRNG_BM_LAYOUT=0;CBRNG_BM_LAYOUT=5").split(";") if s]
     out = []
     for rep in range(int(os.environ.get("TUNE_REPS", "2"))):
         for st in sets:
