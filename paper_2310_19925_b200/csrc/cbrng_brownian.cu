@@ -186,7 +186,8 @@ __global__ void __launch_bounds__(256, MINB) brownian_steps_kernel(const __grid_
 // per particle; threads past n take part in the table and the barriers only.
 constexpr int BR_TAB = 256;
 
-template <bool FOLD, int MINB>
+// SPLIT: Philox mulhilo as IMAD.HI + IMAD (mulhilo_c), tuning build only.
+template <bool FOLD, int MINB, bool SPLIT = false>
 __global__ void __launch_bounds__(256, MINB) brownian_fused_philox_kernel(const __grid_constant__ BrownArgs a) {
     __shared__ uint4 tab[BR_TAB];
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(256, MINB) brownian_fused_philox_kernel(const 
         __syncthreads();
         const uint32_t m = nsteps - base < (uint32_t)BR_TAB ? nsteps - base : (uint32_t)BR_TAB;
 #pragma unroll 2  // steps s and s+1 interleave (the cipher of s+1 under the FP64 chain of s): +3.5 %, r1t_tune.md
-        for (uint32_t s = 0; s < m; s++) step_update<FOLD>(x, y, vx, vy, philox_particle_block_u(P, tab[s]), a);
+        for (uint32_t s = 0; s < m; s++) step_update<FOLD>(x, y, vx, vy, philox_particle_block_u<SPLIT>(P, tab[s]), a);
     }
     if (live) { a.x[i] = x; a.y[i] = y; a.vx[i] = vx; a.vy[i] = vy; }
 }
@@ -326,6 +327,9 @@ static int launch_steps_kb(BrownArgs a, int mode, cudaStream_t st) {
         if (mode == CBRNG_BROWNIAN_FUSED && tab == 1) k = brownian_fused_philox_kernel<FOLD, MINB>;
         if constexpr (TUNING) {  // per-warp tables: 1 % slower (profiles/r2c_tune.md), tuning build only
             if (mode == CBRNG_BROWNIAN_FUSED && tab == 2) k = brownian_fused_philox_wtab_kernel<FOLD, MINB>;
+            static const int split = tuning_knob("CBRNG_BROWNIAN_SPLIT", 0, 0, 2);
+            if (mode == CBRNG_BROWNIAN_FUSED && tab == 1 && split == 1) k = brownian_fused_philox_kernel<FOLD, MINB, true>;
+            if (mode == CBRNG_BROWNIAN_FUSED && tab == 1 && split == 2) k = brownian_fused_philox_kernel<FOLD, 4, true>;
         }
     }
     // One thread per particle: the fused kernel needs every particle resident

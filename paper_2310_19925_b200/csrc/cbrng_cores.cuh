@@ -248,6 +248,7 @@ __device__ __forceinline__ uint4 philox_particle_block(const PhiloxParticle<HI0>
 // M0*ctr and round 1's M1*c2 are the same for every thread of a step. The
 // fused Brownian kernel computes them once per step per CTA (u = {-, lo(M0*ctr),
 // hi(M1*c2), lo(M1*c2)}) and each particle starts at round 1's xors.
+template <bool SPLIT = false>
 __device__ __forceinline__ uint4 philox_particle_block_u(const PhiloxParticle<true>& p, uint4 u) {
     uint32_t c0 = u.z ^ p.k0[1];  // c1 of round 0 == 0
     uint32_t c1 = u.w;
@@ -255,15 +256,15 @@ __device__ __forceinline__ uint4 philox_particle_block_u(const PhiloxParticle<tr
     uint32_t c3;
     {
         uint32_t h0, l0, h1, l1;
-        mulhilo(PHILOX_M0, c0, h0, l0);
-        mulhilo(PHILOX_M1, c2, h1, l1);
+        mulhilo_c<PHILOX_M0, SPLIT>(c0, h0, l0);
+        mulhilo_c<PHILOX_M1, SPLIT>(c2, h1, l1);
         c0 = h1 ^ c1 ^ p.k0[2];
         c1 = l1;
         c2 = h0 ^ p.r2;
         c3 = l0;
     }
 #pragma unroll
-    for (int r = 3; r < 10; r++) philox_round(c0, c1, c2, c3, p.k0[r], p.K1(r));
+    for (int r = 3; r < 10; r++) philox_round_d<SPLIT>(c0, c1, c2, c3, p.k0[r], p.K1(r));
     return make_uint4(c0, c1, c2, c3);
 }
 
@@ -575,10 +576,26 @@ __device__ __forceinline__ uint64_t squares_r1(uint64_t x) {
 }
 
 // Rounds 2-4 from round 1's r (swapped into (h, l) = (lo r, hi r)), y = x, z = x + key.
+// The squaring with the 64-bit addend on the ALU pipe: a plain IMAD.WIDE
+// (no addend: 31.6 thread-ops/clk/SM against 25.2 with one, r1zd probes),
+// then lo + a_lo (IADD3, carry out) and hi + a_hi + carry + 2t (IADD3.X + IADD3).
+__device__ __forceinline__ void squares_sq_swap_alu(uint32_t &h, uint32_t &l, uint64_t a) {
+    uint32_t plo, phi;
+    asm("{.reg .b64 p;\n\tmul.wide.u32 p, %2, %2;\n\tmov.b64 {%0, %1}, p;}" : "=r"(plo), "=r"(phi) : "r"(l));
+    const uint32_t t = mul_lo_opaque(l, h);
+    uint32_t lo, hi;
+    asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;" : "=r"(lo), "=r"(hi)
+        : "r"(plo), "r"(phi), "r"((uint32_t)a), "r"((uint32_t)(a >> 32)));
+    h = lo;
+    l = hi + t + t;
+}
+
+// Rounds 2-4; F = bit mask of rounds 2 (1) / 3 (2) computed with squares_sq_swap_alu.
+template <int F = 0>
 __device__ __forceinline__ uint32_t squares_rounds_234(uint64_t r, uint64_t y, uint64_t z) {
     uint32_t h = (uint32_t)r, l = (uint32_t)(r >> 32);
-    squares_sq_swap(h, l, z);
-    squares_sq_swap(h, l, y);
+    if constexpr (F & 1) squares_sq_swap_alu(h, l, z); else squares_sq_swap(h, l, z);
+    if constexpr (F & 2) squares_sq_swap_alu(h, l, y); else squares_sq_swap(h, l, y);
     const uint64_t p = (uint64_t)l * l + z;
     const uint32_t t = mul_lo_opaque(l, h);
     return (uint32_t)(p >> 32) + t + t;
@@ -619,6 +636,7 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 // E_1, E_2 are folded into 3-input adds, r_2 = r_1 + E_0 + 2 key^2 and
 // r_3 = r_2 + E_0 + 4 key^2, which ptxas cannot put on IMAD.X.
 // z_k = x_k + key = x_{k+1}. k2x2 = 2 key^2, k2x4 = 4 key^2.
+template <int F = 0>
 __device__ __forceinline__ uint4 squares_x4_inc(uint64_t x0, uint64_t e0, uint64_t key, uint64_t k2x2, uint64_t k2x4,
                                                 uint64_t *x4_out = nullptr) {
     const uint64_t x1 = add64_alu(x0, key), x2 = add64_alu(x1, key), x3 = add64_alu(x2, key);
@@ -626,8 +644,8 @@ __device__ __forceinline__ uint4 squares_x4_inc(uint64_t x0, uint64_t e0, uint64
     if (x4_out) *x4_out = x4;
     const uint64_t r0 = squares_r1(x0);
     const uint64_t r1 = add64_alu(r0, e0), r2 = add64_3(r1, e0, k2x2), r3 = add64_3(r2, e0, k2x4);
-    return make_uint4(squares_rounds_234(r0, x0, x1), squares_rounds_234(r1, x1, x2), squares_rounds_234(r2, x2, x3),
-                      squares_rounds_234(r3, x3, x4));
+    return make_uint4(squares_rounds_234<F>(r0, x0, x1), squares_rounds_234<F>(r1, x1, x2),
+                      squares_rounds_234<F>(r2, x2, x3), squares_rounds_234<F>(r3, x3, x4));
 }
 
 __device__ __forceinline__ uint32_t squares_stream_word(const SquaresStream &p, uint32_t bc) {

@@ -39,13 +39,19 @@ struct FillArgs {
 
 // CV: where the f32 map's shift / convert / scale run (u32_to_f32_cv).
 // BV: the lane's view of the Box-Muller tables (OUT_NORMAL only).
+// CV & 8 (tuning build, CBRNG_NOSTORE=1): HBM-free ceiling of the same kernel.
+// Unit u is stored at u mod 2^16 (a 1-2 MB ring that stays in L2), so the
+// instruction stream is the product's plus one LOP3 per store, and no output
+// reaches HBM. (A value-dependent store predicate instead splits the unrolled
+// tile into branches and serialises it.)
 template <int OUT, int CV = 0, class BV = BmView<>>
 __device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0,
                                            const BV &bm = BV{}) {
+    if constexpr ((CV & 8) != 0) u &= 0xFFFFu;
     if constexpr (OUT == OUT_U32) {
         __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
     } else if constexpr (OUT == OUT_F32) {
-        __stcs(reinterpret_cast<float4 *>(out0) + u, u32x4_to_f32x4<CV>(w, m24));
+        __stcs(reinterpret_cast<float4 *>(out0) + u, u32x4_to_f32x4<CV & 7>(w, m24));
     } else if constexpr (OUT == OUT_F64) {
         __stcs(reinterpret_cast<double2 *>(out0) + u, make_double2(u32x2_to_f64(w.x, w.y), u32x2_to_f64(w.z, w.w)));
     } else {
@@ -104,7 +110,7 @@ __device__ __forceinline__ void fill_job(const FillArgs<ALG> &a, uint64_t warp, 
     for (uint64_t t = PIPE ? n_full : warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
-        if constexpr (ALG == SQUARES && V == 2) {
+        if constexpr (ALG == SQUARES && V >= 2) {
             // no counter wrap, round 1 by finite differences (squares_x4_inc):
             // x and E for the lane's first unit, then +128 counters per j
             const uint32_t c0 = a.bc0 + 4u * (uint32_t)base;
@@ -113,7 +119,8 @@ __device__ __forceinline__ void fill_job(const FillArgs<ALG> &a, uint64_t warp, 
             const uint64_t sx = a.p.key << 7, se = a.p.k2x2 << 7;
 #pragma unroll
             for (int j = 0; j < ILP; j++) {
-                w[j] = squares_x4_inc(x, e, a.p.key, a.p.k2x2, a.p.k2x4);
+                // V 3/4/5 (tuning): rounds 2 / 3 / both with the addend on the ALU pipe
+                w[j] = squares_x4_inc<V - 2>(x, e, a.p.key, a.p.k2x2, a.p.k2x4);
                 x = add64_alu(x, sx);
                 e = add64_alu(e, se);
             }
@@ -158,14 +165,14 @@ __global__ void __launch_bounds__(256, MB) fill_kernel(const __grid_constant__ F
 // Box-Muller fill: NT threads per CTA, LC / SC interleaved copies of the log /
 // sincos tables in shared memory (cbrng_bm.cuh), MB CTAs per SM for the
 // register allocator.
-template <int ALG, int ILP, bool SKIP, int V, int LC, int SC, int NT, int MB, bool PIPE = false>
+template <int ALG, int ILP, bool SKIP, int V, int LC, int SC, int NT, int MB, bool PIPE = false, int CV = 0>
 __global__ void __launch_bounds__(NT, MB) normal_fill_kernel(const __grid_constant__ FillArgs<ALG> a) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     extern __shared__ __align__(16) unsigned char s_dyn[];
     const BmView<LC, SC> v = bm_stage_table(reinterpret_cast<BmTables<LC, SC> *>(s_dyn));
-    fill_job<ALG, OUT_NORMAL, ILP, SKIP, V, 0, BmView<LC, SC>, PIPE>(a, warp, nwarps, lane, v);
+    fill_job<ALG, OUT_NORMAL, ILP, SKIP, V, CV, BmView<LC, SC>, PIPE>(a, warp, nwarps, lane, v);
 }
 
 // Several counter-based fills in one launch (cbrng_words_multi /
@@ -259,6 +266,9 @@ constexpr int FILL_BLOCK = 256;
 template <int ALG, int OUT, bool SKIP, int ILP, int V, int CV, int MB = 0>
 static int launch_fill_ilp(const FillArgs<ALG> &a, cudaStream_t st) {
     auto k = fill_kernel<ALG, OUT, ILP, SKIP, V, CV, MB>;
+    if constexpr (TUNING && !SKIP) {
+        if (tuning_knob("CBRNG_NOSTORE", 0, 0, 1)) k = fill_kernel<ALG, OUT, ILP, SKIP, V, CV | 8, MB>;
+    }
     uint64_t work = (a.n_units + (FILL_BLOCK * ILP) - 1) / (FILL_BLOCK * ILP);
     unsigned grid = grid_for(k, FILL_BLOCK, 0, work ? work : 1);
     k<<<grid, FILL_BLOCK, 0, st>>>(a);
@@ -292,6 +302,9 @@ constexpr int BM_ILP = 8, BM_LC = 8, BM_SC = 2, BM_NT = 1024, BM_MB = 2, BM_LAYO
 template <int ALG, bool SKIP, int V, int ILP, int LC, int SC, int NT, int MB, bool PIPE = false>
 static int launch_normal(const FillArgs<ALG> &a, cudaStream_t st) {
     auto k = normal_fill_kernel<ALG, ILP, SKIP, V, LC, SC, NT, MB, PIPE>;
+    if constexpr (TUNING && !SKIP) {
+        if (tuning_knob("CBRNG_NOSTORE", 0, 0, 1)) k = normal_fill_kernel<ALG, ILP, SKIP, V, LC, SC, NT, MB, PIPE, 8>;
+    }
     constexpr size_t smem = sizeof(BmTables<LC, SC>);
     // per launch: the attribute is per device and the ABI serves any current device
     if (smem > 48 * 1024) {
@@ -395,8 +408,11 @@ static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
         if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) {
             // V 2: round 1 by finite differences (tuning: CBRNG_SQ_INC=0 -> V 1)
             if constexpr (TUNING) {
-                static const bool inc = tuning_knob("CBRNG_SQ_INC", 1, 0, 1) == 1;
-                if (!inc) return launch_fill_cv<ALG, OUT, SKIP, 1>(a, st);
+                static const int inc = tuning_knob("CBRNG_SQ_INC", 1, 0, 4);
+                if (inc == 0) return launch_fill_cv<ALG, OUT, SKIP, 1>(a, st);
+                if (inc == 2) return launch_fill_cv<ALG, OUT, SKIP, 3>(a, st);
+                if (inc == 3) return launch_fill_cv<ALG, OUT, SKIP, 4>(a, st);
+                if (inc == 4) return launch_fill_cv<ALG, OUT, SKIP, 5>(a, st);
             }
             return launch_fill_cv<ALG, OUT, SKIP, 2>(a, st);
         }

@@ -75,9 +75,10 @@ def test_threefry_variants(v):
     assert _run({"CBRNG_TF_VARIANT": str(v)}) == []
 
 
-@pytest.mark.parametrize("inc", [0, 1])
+@pytest.mark.parametrize("inc", [0, 1, 2, 3, 4])
 def test_squares_round1_forms(inc):
-    """Squares round 1 as one 64-bit square per word (0) or by finite differences (1)."""
+    """Squares round 1 as one 64-bit square per word (0) or by finite differences (1; 2-4: rounds 2/3/both
+    with the 64-bit addend on the ALU pipe)."""
     assert _run({"CBRNG_SQ_INC": str(inc)}) == []
 
 
@@ -176,6 +177,7 @@ print(json.dumps(bad))
     {"CBRNG_BROWNIAN_TAB": "0"}, {"CBRNG_BROWNIAN_TAB": "2"}, {"CBRNG_BROWNIAN_PINGPONG": "0"}, {"CBRNG_BROWNIAN_PDL": "0"},
     {"CBRNG_GRID_MULT": "0"}, {"CBRNG_GRID_MULT": "16"}, {"CBRNG_TY_GRID": "8"}, {"CBRNG_BM_GRID": "4"},
     *({"CBRNG_BM_LAYOUT": str(k)} for k in range(13)), {"CBRNG_BM_SPLIT": "1"},
+    {"CBRNG_BROWNIAN_SPLIT": "1"}, {"CBRNG_BROWNIAN_SPLIT": "2"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_misc_knobs(env):
     import torch

@@ -154,10 +154,15 @@ def _add(a: dict, b: dict, w: float) -> dict:
 
 def fill_work(so: str, alg: int, out: int) -> dict:
     """Per word (OUT 0/1/2 words: 4 per unit) or per pair (OUT 3) of the block-aligned fill."""
-    # Squares: the non-wrapping finite-difference variant (V 2) is the bulk path
+    # Squares: the non-wrapping finite-difference variant (V 2) is the bulk path;
+    # Box-Muller (OUT 3): normal_fill_kernel<ALG, ILP, SKIP, V, LC, SC, NT, MB, PIPE, CV>
     v = "2" if alg == 2 else r"\d+"
-    name, ins = find(so, rf"fill_kernel<{alg}, {out}, (\d+), false, {v},")
-    ilp = int(re.search(rf"fill_kernel<{alg}, {out}, (\d+),", name).group(1))
+    if out == 3:
+        name, ins = find(so, rf"normal_fill_kernel<{alg}, (\d+), false, {v}, \d+, \d+, \d+, \d+, false, 0>")
+        ilp = int(re.search(rf"normal_fill_kernel<{alg}, (\d+),", name).group(1))
+    else:
+        name, ins = find(so, rf"fill_kernel<{alg}, {out}, (\d+), false, {v},")
+        ilp = int(re.search(rf"fill_kernel<{alg}, {out}, (\d+),", name).group(1))
     lo, hi = hot_loop(ins)
     per = ilp if out == 3 else 4 * ilp
     return {"kernel": name, "unit": "pair" if out == 3 else "word", "loop": [hex(lo), hex(hi)],
