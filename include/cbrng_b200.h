@@ -146,6 +146,26 @@ int cbrng_tyche_mix(uint32_t *state, uint64_t n, uint32_t rounds, void *stream);
 int cbrng_tyche_init(const uint64_t *seeds, uint64_t seed_base, const uint32_t *ctrs, uint32_t ctr_scalar,
                      uint64_t n, uint32_t *state, void *stream);
 
+/* ---------------- scalar calls (generators.py:101-224, 295-320) ----------------
+ * One synchronous round trip for the reference's scalar API: args and the result
+ * are HOST memory; the library stages them through a mapped pinned buffer and
+ * runs the vector kernels above on one lane on an internal per-device stream.
+ * nargs / nout per op:
+ *   PHILOX_BLOCK   ctr0..3, key0..1                      -> 4 words   (generators.py:101-122)
+ *   THREEFRY_BLOCK ctr0..3, key0..3, rounds              -> 4 words   (generators.py:125-154)
+ *   SQUARES_KEY    seed                                  -> key lo, hi (generators.py:157-170)
+ *   SQUARES_ROUND  key, ctr                              -> 1 word    (generators.py:173-187)
+ *   TYCHE_INIT     seed, stream_ctr                      -> state[4]  (generators.py:190-218)
+ *   TYCHE_MIX      state0..3, rounds                     -> state[4]  (generators.py:201-210)
+ *   STREAM_WORDS   alg (0-2), seed, stream_ctr, word_pos -> nout words (<= 2^18) of cbrng_words
+ *   TYCHE_WORDS    state0..3                             -> nout-4 words, then the state after them */
+enum {
+    CBRNG_SCALAR_PHILOX_BLOCK = 0, CBRNG_SCALAR_THREEFRY_BLOCK = 1, CBRNG_SCALAR_SQUARES_KEY = 2,
+    CBRNG_SCALAR_SQUARES_ROUND = 3, CBRNG_SCALAR_TYCHE_INIT = 4, CBRNG_SCALAR_TYCHE_MIX = 5,
+    CBRNG_SCALAR_STREAM_WORDS = 6, CBRNG_SCALAR_TYCHE_WORDS = 7
+};
+int cbrng_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, uint64_t nout);
+
 /* ---------------- Brownian walk (brownian.py) ----------------
  * SoA float64 particle arrays [dev]. pid == NULL -> pid[i] = pid_base + i. */
 /* init_particles (brownian.py:112-126) */

@@ -53,6 +53,7 @@ SIGNATURES = {
     "cbrng_squares_keys": (i32, [vp, u64, vp, vp]),
     "cbrng_tyche_mix": (i32, [vp, u64, u32, vp]),
     "cbrng_tyche_init": (i32, [vp, u64, vp, u32, u64, vp, vp]),
+    "cbrng_scalar": (i32, [i32, vp, u32, vp, u64]),
     "cbrng_brownian_init": (i32, [i32, u64, vp, u64, u32, vp, vp, vp, vp, vp]),
     "cbrng_brownian_steps": (i32, [i32, u64, vp, u64, vp, vp, vp, vp, u32, u64, u64, f64, f64, f64, i32, vp]),
     "cbrng_brownian_stats": (i32, [u64, vp, u64, vp, vp, vp, vp, vp, vp]),
@@ -138,6 +139,29 @@ def curand_lib():
             if _curand is None:
                 _curand = _bind(CURAND_LIB_PATH, CURAND_SIGNATURES)
     return _curand
+
+
+# cbrng_scalar ops (include/cbrng_b200.h)
+(SCALAR_PHILOX_BLOCK, SCALAR_THREEFRY_BLOCK, SCALAR_SQUARES_KEY, SCALAR_SQUARES_ROUND, SCALAR_TYCHE_INIT,
+ SCALAR_TYCHE_MIX, SCALAR_STREAM_WORDS, SCALAR_TYCHE_WORDS) = range(8)
+SCALAR_MAX_WORDS = 1 << 18
+_scalar_tls = threading.local()
+
+
+def scalar(op: int, args, nout: int):
+    """One synchronous scalar round trip through cbrng_scalar (host args, host
+    result): a uint32 numpy array of nout words. Used by the reference's scalar
+    API (block functions, generator windows); the GPU computes every word."""
+    import numpy as np
+
+    buf = getattr(_scalar_tls, "args", None)
+    if buf is None:
+        buf = _scalar_tls.args = (C.c_uint64 * 16)()
+    for i, a in enumerate(args):
+        buf[i] = int(a) & 0xFFFFFFFFFFFFFFFF
+    out = np.empty(nout, np.uint32)
+    check(lib().cbrng_scalar(op, buf, len(args), out.ctypes.data, nout), "cbrng_scalar")
+    return out
 
 
 def last_error() -> str:

@@ -576,33 +576,17 @@ __device__ __forceinline__ uint64_t squares_r1(uint64_t x) {
 }
 
 // Rounds 2-4 from round 1's r (swapped into (h, l) = (lo r, hi r)), y = x, z = x + key.
-// The squaring with the 64-bit addend on the ALU pipe: a plain IMAD.WIDE
-// (no addend: 31.6 thread-ops/clk/SM against 25.2 with one, r1zd probes),
-// then lo + a_lo (IADD3, carry out) and hi + a_hi + carry + 2t (IADD3.X + IADD3).
-__device__ __forceinline__ void squares_sq_swap_alu(uint32_t &h, uint32_t &l, uint64_t a) {
-    uint32_t plo, phi;
-    asm("{.reg .b64 p;\n\tmul.wide.u32 p, %2, %2;\n\tmov.b64 {%0, %1}, p;}" : "=r"(plo), "=r"(phi) : "r"(l));
-    const uint32_t t = mul_lo_opaque(l, h);
-    uint32_t lo, hi;
-    asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;" : "=r"(lo), "=r"(hi)
-        : "r"(plo), "r"(phi), "r"((uint32_t)a), "r"((uint32_t)(a >> 32)));
-    h = lo;
-    l = hi + t + t;
-}
-
-// Rounds 2-4; F = bit mask of rounds 2 (1) / 3 (2) computed with squares_sq_swap_alu.
-template <int F = 0>
 __device__ __forceinline__ uint32_t squares_rounds_234(uint64_t r, uint64_t y, uint64_t z) {
     uint32_t h = (uint32_t)r, l = (uint32_t)(r >> 32);
-    if constexpr (F & 1) squares_sq_swap_alu(h, l, z); else squares_sq_swap(h, l, z);
-    if constexpr (F & 2) squares_sq_swap_alu(h, l, y); else squares_sq_swap(h, l, y);
+    squares_sq_swap(h, l, z);
+    squares_sq_swap(h, l, y);
     const uint64_t p = (uint64_t)l * l + z;
     const uint32_t t = mul_lo_opaque(l, h);
     return (uint32_t)(p >> 32) + t + t;
 }
 
 // An opaque zero in the constant bank: ptxas cannot fold it, and IADD3 takes
-// it as a c[] operand (no register).
+// it as a c[] operand (no register). Tuning-build variants only (squares_x4_inc<true>).
 static __constant__ uint32_t c_zero = 0;
 
 // 64-bit a + b whose high half is a 3-input add against an opaque zero
@@ -633,19 +617,26 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 // E_k = 2 key x_k + key^2 + key and E_{k+1} = E_k + 2 key^2 (all mod 2^64), so
 // three of the four round-1 squarings (an IMAD.WIDE + IMAD each on the
 // FMA-heavy pipe, which bounds Squares) become 64-bit adds on the ALU pipe.
-// E_1, E_2 are folded into 3-input adds, r_2 = r_1 + E_0 + 2 key^2 and
-// r_3 = r_2 + E_0 + 4 key^2, which ptxas cannot put on IMAD.X.
-// z_k = x_k + key = x_{k+1}. k2x2 = 2 key^2, k2x4 = 4 key^2.
-template <int F = 0>
+// z_k = x_k + key = x_{k+1}. k2x2 = 2 key^2, k2x4 = 4 key^2; x4_out <- x_4.
+// ALUC (tuning build): every carry add forced onto the ALU pipe (add64_alu /
+// add64_3: E_1, E_2 folded into 3-input adds). It removes 9 % of the
+// FMA-heavy slots (IMAD.X) and measured 2 % slower (profiles/r2d_tune.md).
+template <bool ALUC = false>
 __device__ __forceinline__ uint4 squares_x4_inc(uint64_t x0, uint64_t e0, uint64_t key, uint64_t k2x2, uint64_t k2x4,
                                                 uint64_t *x4_out = nullptr) {
-    const uint64_t x1 = add64_alu(x0, key), x2 = add64_alu(x1, key), x3 = add64_alu(x2, key);
-    const uint64_t x4 = add64_alu(x3, key);
-    if (x4_out) *x4_out = x4;
+    uint64_t x1, x2, x3, x4, r1, r2, r3;
     const uint64_t r0 = squares_r1(x0);
-    const uint64_t r1 = add64_alu(r0, e0), r2 = add64_3(r1, e0, k2x2), r3 = add64_3(r2, e0, k2x4);
-    return make_uint4(squares_rounds_234<F>(r0, x0, x1), squares_rounds_234<F>(r1, x1, x2),
-                      squares_rounds_234<F>(r2, x2, x3), squares_rounds_234<F>(r3, x3, x4));
+    if constexpr (ALUC) {
+        x1 = add64_alu(x0, key), x2 = add64_alu(x1, key), x3 = add64_alu(x2, key), x4 = add64_alu(x3, key);
+        r1 = add64_alu(r0, e0), r2 = add64_3(r1, e0, k2x2), r3 = add64_3(r2, e0, k2x4);
+    } else {
+        x1 = add64_opaque(x0, key), x2 = add64_opaque(x1, key), x3 = add64_opaque(x2, key), x4 = add64_opaque(x3, key);
+        const uint64_t e1 = add64_opaque(e0, k2x2), e2 = add64_opaque(e1, k2x2);
+        r1 = add64_opaque(r0, e0), r2 = add64_opaque(r1, e1), r3 = add64_opaque(r2, e2);
+    }
+    if (x4_out) *x4_out = x4;
+    return make_uint4(squares_rounds_234(r0, x0, x1), squares_rounds_234(r1, x1, x2), squares_rounds_234(r2, x2, x3),
+                      squares_rounds_234(r3, x3, x4));
 }
 
 __device__ __forceinline__ uint32_t squares_stream_word(const SquaresStream &p, uint32_t bc) {

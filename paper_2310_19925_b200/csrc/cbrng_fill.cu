@@ -110,19 +110,24 @@ __device__ __forceinline__ void fill_job(const FillArgs<ALG> &a, uint64_t warp, 
     for (uint64_t t = PIPE ? n_full : warp; t < n_full; t += nwarps) {
         const uint64_t base = t * TILE + lane;
         uint4 w[ILP];
-        if constexpr (ALG == SQUARES && V >= 2) {
+        if constexpr (ALG == SQUARES && (V == 2 || V == 6)) {
             // no counter wrap, round 1 by finite differences (squares_x4_inc):
             // x and E for the lane's first unit, then +128 counters per j
+            // (V 6, tuning: carries forced onto the ALU pipe)
             const uint32_t c0 = a.bc0 + 4u * (uint32_t)base;
             uint64_t x = (uint64_t)c0 * a.p.key + a.p.base;
             uint64_t e = (uint64_t)c0 * a.p.k2x2 + a.p.ebase;
             const uint64_t sx = a.p.key << 7, se = a.p.k2x2 << 7;
 #pragma unroll
             for (int j = 0; j < ILP; j++) {
-                // V 3/4/5 (tuning): rounds 2 / 3 / both with the addend on the ALU pipe
-                w[j] = squares_x4_inc<V - 2>(x, e, a.p.key, a.p.k2x2, a.p.k2x4);
-                x = add64_alu(x, sx);
-                e = add64_alu(e, se);
+                w[j] = squares_x4_inc<V == 6>(x, e, a.p.key, a.p.k2x2, a.p.k2x4);
+                if constexpr (V == 6) {
+                    x = add64_alu(x, sx);
+                    e = add64_alu(e, se);
+                } else {
+                    x = add64_opaque(x, sx);
+                    e = add64_opaque(e, se);
+                }
             }
         } else if constexpr (ALG == SQUARES && V == 1) {
             // no counter wrap anywhere in the fill: unit u's first product
@@ -373,9 +378,11 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
             static const int split = tuning_knob("CBRNG_BM_SPLIT", 0, 0, 1);
             static const int lay = tuning_knob("CBRNG_BM_LAYOUT", BM_LAYOUT_DEFAULT, 0, 12);
             return split ? launch_normal_layout<ALG, SKIP, 1>(a, st, lay) : launch_normal_layout<ALG, SKIP, V>(a, st, lay);
+        } else if constexpr (ALG != PHILOX) {
+            return launch_normal<ALG, SKIP, V, 4, 8, 2, 512, 0>(a, st);  // wider cipher state
+        } else {
+            return launch_normal<ALG, SKIP, V, BM_ILP, BM_LC, BM_SC, BM_NT, BM_MB>(a, st);
         }
-        if constexpr (ALG != PHILOX) return launch_normal<ALG, SKIP, V, 4, 8, 2, 512, 0>(a, st);  // wider cipher state
-        return launch_normal<ALG, SKIP, V, BM_ILP, BM_LC, BM_SC, BM_NT, BM_MB>(a, st);
     } else {
         return launch_fill_ilp<ALG, OUT, SKIP, 8, V, CV>(a, st);
     }
@@ -408,11 +415,10 @@ static int launch_fill_k(const FillArgs<ALG> &a, cudaStream_t st) {
         if ((uint64_t)a.bc0 + 4ull * (a.n_units + 1) <= (1ull << 32)) {
             // V 2: round 1 by finite differences (tuning: CBRNG_SQ_INC=0 -> V 1)
             if constexpr (TUNING) {
-                static const int inc = tuning_knob("CBRNG_SQ_INC", 1, 0, 4);
+                // CBRNG_SQ_INC: 0 -> V 1 (no finite differences), 2 -> V 6 (ALU-forced carries)
+                static const int inc = tuning_knob("CBRNG_SQ_INC", 1, 0, 2);
                 if (inc == 0) return launch_fill_cv<ALG, OUT, SKIP, 1>(a, st);
-                if (inc == 2) return launch_fill_cv<ALG, OUT, SKIP, 3>(a, st);
-                if (inc == 3) return launch_fill_cv<ALG, OUT, SKIP, 4>(a, st);
-                if (inc == 4) return launch_fill_cv<ALG, OUT, SKIP, 5>(a, st);
+                if (inc == 2) return launch_fill_cv<ALG, OUT, SKIP, 6>(a, st);
             }
             return launch_fill_cv<ALG, OUT, SKIP, 2>(a, st);
         }

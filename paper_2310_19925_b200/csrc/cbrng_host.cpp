@@ -1,6 +1,7 @@
 // cbrng_host.cpp — host-side pieces of the C ABI: version, thread-local error
-// text, launch-geometry cache, and the byte-serial FNV-1a checksum
-// (_kernels.py:89-96), which is sequential by definition and stays on the host.
+// text, launch-geometry cache, the byte-serial FNV-1a checksum
+// (_kernels.py:89-96), which is sequential by definition and stays on the host,
+// and the low-latency scalar transport (cbrng_scalar).
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -64,9 +65,139 @@ int resident_blocks(const void *kernel, int block, size_t smem) {
     return g;
 }
 
+// Scalar transport (cbrng_scalar): per device, one mapped pinned host buffer
+// (inputs at offset 0, outputs at SCALAR_OUT_OFF) and one non-blocking stream.
+// The kernels read their few inputs and write their outputs straight through
+// the mapping, so a call is one launch and one stream synchronisation.
+constexpr size_t SCALAR_OUT_OFF = 4096, SCALAR_OUT_WORDS = 1u << 18;
+struct ScalarCtx {
+    std::mutex mu;
+    uint8_t *host = nullptr;
+    uint8_t *dev = nullptr;
+    cudaStream_t st = nullptr;
+};
+
+static ScalarCtx *scalar_ctx(int &rc) {
+    static std::mutex mu;
+    static ScalarCtx *ctx[64] = {};
+    int d = 0;
+    rc = check_cuda(cudaGetDevice(&d), "cudaGetDevice");
+    if (rc) return nullptr;
+    if (d < 0 || d >= 64) {
+        set_error("device %d out of range", d);
+        rc = CBRNG_EINVAL;
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> g(mu);
+    if (!ctx[d]) {
+        auto *c = new ScalarCtx;
+        void *h = nullptr, *dp = nullptr;
+        rc = check_cuda(cudaHostAlloc(&h, SCALAR_OUT_OFF + 4 * SCALAR_OUT_WORDS, cudaHostAllocMapped | cudaHostAllocPortable),
+                        "cudaHostAlloc (scalar buffer)");
+        if (!rc) rc = check_cuda(cudaHostGetDevicePointer(&dp, h, 0), "cudaHostGetDevicePointer");
+        if (!rc) rc = check_cuda(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (rc) {
+            if (h) cudaFreeHost(h);
+            delete c;
+            return nullptr;
+        }
+        c->host = static_cast<uint8_t *>(h);
+        c->dev = static_cast<uint8_t *>(dp);
+        ctx[d] = c;
+    }
+    return ctx[d];
+}
+
 }  // namespace cbrng
 
 extern "C" {
+
+int cbrng_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, uint64_t nout) {
+    using namespace cbrng;
+    clear_error();
+    static const uint32_t NARGS[8] = {6, 9, 1, 2, 2, 5, 4, 4};
+    static const uint64_t NOUT[6] = {4, 4, 2, 1, 4, 4};
+    if (op < 0 || op > 7) {
+        set_error("unknown scalar op %d", op);
+        return CBRNG_EINVAL;
+    }
+    if (nargs != NARGS[op] || (nargs && !args) || (nout && !out)) {
+        set_error("scalar op %d: expects %u args and an output buffer", op, NARGS[op]);
+        return CBRNG_EINVAL;
+    }
+    if (op < 6 ? nout != NOUT[op] : (op == 6 ? nout > SCALAR_OUT_WORDS : (nout < 4 || nout > SCALAR_OUT_WORDS))) {
+        set_error("scalar op %d: bad output length %llu", op, (unsigned long long)nout);
+        return CBRNG_EINVAL;
+    }
+    int rc = 0;
+    ScalarCtx *c = scalar_ctx(rc);
+    if (!c) return rc;
+    std::lock_guard<std::mutex> g(c->mu);
+    uint32_t *in32 = reinterpret_cast<uint32_t *>(c->host);
+    uint64_t *in64 = reinterpret_cast<uint64_t *>(c->host);
+    const uint32_t *din32 = reinterpret_cast<const uint32_t *>(c->dev);
+    const uint64_t *din64 = reinterpret_cast<const uint64_t *>(c->dev);
+    uint32_t *hout = reinterpret_cast<uint32_t *>(c->host + SCALAR_OUT_OFF);
+    uint32_t *dout = reinterpret_cast<uint32_t *>(c->dev + SCALAR_OUT_OFF);
+    void *st = c->st;
+    switch (op) {
+        case CBRNG_SCALAR_PHILOX_BLOCK:  // ctr[4], key[2] (u32 each)
+            for (int i = 0; i < 6; i++) in32[i] = (uint32_t)args[i];
+            rc = cbrng_philox4x32(din32, din32 + 4, 1, dout, st);
+            break;
+        case CBRNG_SCALAR_THREEFRY_BLOCK:  // ctr[4], key[4], rounds
+            for (int i = 0; i < 8; i++) in32[i] = (uint32_t)args[i];
+            rc = cbrng_threefry4x32(din32, din32 + 4, (int)args[8], 1, dout, st);
+            break;
+        case CBRNG_SCALAR_SQUARES_KEY:  // seed -> key (lo, hi)
+            in64[0] = args[0];
+            rc = cbrng_squares_keys(din64, 1, reinterpret_cast<uint64_t *>(dout), st);
+            break;
+        case CBRNG_SCALAR_SQUARES_ROUND:  // key, ctr
+            in64[0] = args[1];
+            in64[1] = args[0];
+            rc = cbrng_squares32(din64, din64 + 1, 1, dout, st);
+            break;
+        case CBRNG_SCALAR_TYCHE_INIT:  // seed, stream counter -> state[4]
+            rc = cbrng_tyche_init(nullptr, args[0], nullptr, (uint32_t)args[1], 1, dout, st);
+            break;
+        case CBRNG_SCALAR_TYCHE_MIX:  // state[4], rounds -> state[4]
+            for (int i = 0; i < 4; i++) hout[i] = (uint32_t)args[i];
+            rc = args[4] ? cbrng_tyche_mix(dout, 1, (uint32_t)args[4], st) : CBRNG_OK;
+            break;
+        case CBRNG_SCALAR_STREAM_WORDS:  // alg, seed, stream counter, word position -> nout words
+            if (args[0] > 2) {
+                set_error("scalar stream words: counter-based generators only (alg %llu)", (unsigned long long)args[0]);
+                return CBRNG_EALG;
+            }
+            rc = nout ? cbrng_words((int)args[0], args[1], (uint32_t)args[2], args[3], nullptr, nout, dout, nullptr, st)
+                      : CBRNG_OK;
+            break;
+        default: {  // CBRNG_SCALAR_TYCHE_WORDS: state[4] -> nout - 4 words, then the state after them
+            uint32_t s4[4];
+            for (int i = 0; i < 4; i++) s4[i] = (uint32_t)args[i];
+            const uint64_t n = nout - 4;
+            if (n) {
+                rc = cbrng_words(3, 0, 0, 0, s4, n, dout, dout + ((n + 3) & ~3ull), st);
+            } else {
+                for (int i = 0; i < 4; i++) hout[i] = s4[i];
+            }
+            break;
+        }
+    }
+    if (rc) return rc;
+    rc = check_cuda(cudaStreamSynchronize(c->st), "scalar call");
+    if (rc) return rc;
+    if (op == CBRNG_SCALAR_TYCHE_WORDS && nout > 4) {
+        const uint64_t n = nout - 4;
+        std::memcpy(out, hout, 4 * n);
+        std::memcpy(out + n, hout + ((n + 3) & ~3ull), 16);
+    } else {
+        std::memcpy(out, hout, 4 * nout);
+    }
+    return CBRNG_OK;
+}
+
 
 const char *cbrng_version(void) { return "cbrng-b200 0.1.0 (sm_100a)"; }
 

@@ -145,7 +145,7 @@ template <> struct RowGen<SQUARES> {
     }
     __device__ __forceinline__ uint4 next4() {
         const uint4 w = squares_x4_inc(x, e, key, k2x2, k2x4, &x);  // x <- x_4, the next call's x_0
-        e = add64_alu(e, k2x4 << 1);                                  // E_4 = E_0 + 8 key^2
+        e = add64_opaque(e, k2x4 << 1);                               // E_4 = E_0 + 8 key^2
         return w;
     }
 };

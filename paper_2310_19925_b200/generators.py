@@ -91,45 +91,46 @@ def rotl32(x: int, r: int) -> int:
     return ((x << r) | (x >> (32 - r))) & MASK32
 
 
-def philox_block(key, ctr) -> Block:
-    from . import bulk
+# Each is one cbrng_scalar round trip (a one-lane kernel through a mapped pinned
+# buffer, tools/bench_scalar.py).
 
-    out = bulk.philox4x32(*[np.uint32(w & MASK32) for w in ctr], *[np.uint32(w & MASK32) for w in key])
-    return Block(*(int(np.asarray(w).reshape(-1)[0]) for w in out))
+def philox_block(key, ctr) -> Block:
+    from . import _lib
+
+    return Block(*(int(w) for w in _lib.scalar(_lib.SCALAR_PHILOX_BLOCK, [*ctr, *key], 4)))
 
 
 def threefry_block(key, ctr, rounds: int = THREEFRY_ROUNDS) -> Block:
-    from . import bulk
+    from . import _lib
 
-    out = bulk.threefry4x32(*[np.uint32(w & MASK32) for w in ctr], *[np.uint32(w & MASK32) for w in key],
-                            rounds=rounds)
-    return Block(*(int(np.asarray(w).reshape(-1)[0]) for w in out))
+    if rounds < 0:
+        raise ValueError("rounds must be >= 0")
+    return Block(*(int(w) for w in _lib.scalar(_lib.SCALAR_THREEFRY_BLOCK, [*ctr, *key, rounds], 4)))
 
 
 def squares_key(seed: int) -> int:
-    from . import bulk
+    from . import _lib
 
-    return int(np.asarray(bulk.squares_keys(np.uint64(seed & MASK64))).reshape(-1)[0])
+    lo, hi = _lib.scalar(_lib.SCALAR_SQUARES_KEY, [seed & MASK64], 2)
+    return (int(hi) << 32) | int(lo)
 
 
 def squares_round(seed_key: int, counter: int) -> int:
-    from . import bulk
+    from . import _lib
 
-    return int(np.asarray(bulk.squares32(np.uint64(counter & MASK64), np.uint64(seed_key & MASK64))).reshape(-1)[0])
+    return int(_lib.scalar(_lib.SCALAR_SQUARES_ROUND, [seed_key & MASK64, counter & MASK64], 1)[0])
 
 
 def tyche_mix(state) -> tuple[int, int, int, int]:
-    from . import bulk
+    from . import _lib
 
-    out = bulk.tyche_mix(*[np.uint32(w & MASK32) for w in state])
-    return tuple(int(np.asarray(w).reshape(-1)[0]) for w in out)
+    return tuple(int(w) for w in _lib.scalar(_lib.SCALAR_TYCHE_MIX, [*(w & MASK32 for w in state), 1], 4))
 
 
 def tyche_init(seed: int, stream_counter: int) -> tuple[int, int, int, int]:
-    from . import bulk
+    from . import _lib
 
-    out = bulk.tyche_init(np.uint64(seed & MASK64), np.uint32(stream_counter & MASK32))
-    return tuple(int(np.asarray(w).reshape(-1)[0]) for w in out)
+    return tuple(int(w) for w in _lib.scalar(_lib.SCALAR_TYCHE_INIT, [seed & MASK64, stream_counter & MASK32], 4))
 
 
 def tyche_next(state) -> tuple[int, tuple[int, int, int, int]]:
@@ -255,12 +256,13 @@ class Generator:
         if self.algorithm is Algorithm.TYCHE:
             self._tyche_end_state()
             if self._ty_pending.size == 0:
-                from . import bulk
+                from . import _lib
 
                 n = self._pf_n
                 self._pf_n = min(self._pf_n * 2, _PF_MAX)
                 self._ty_base = self._ty_state
-                self._ty_pending, self._ty_state = bulk.tyche_words_from(self._ty_state, n)
+                r = _lib.scalar(_lib.SCALAR_TYCHE_WORDS, self._ty_state, n + 4)
+                self._ty_pending, self._ty_state = r[:n], tuple(int(w) for w in r[n:])
                 self._ty_win = n
             w = int(self._ty_pending[0])
             self._ty_pending = self._ty_pending[1:]
@@ -275,11 +277,11 @@ class Generator:
         return w
 
     def _refill(self, pos: int) -> None:
-        from . import bulk
+        from . import _lib
 
         n = self._pf_n
         self._pf_n = min(self._pf_n * 2, _PF_MAX)
-        self._pf = bulk.stream_words(self.algorithm, self.seed, self.stream_counter, pos, n, device="cpu")
+        self._pf = _lib.scalar(_lib.SCALAR_STREAM_WORDS, [int(self.algorithm), self.seed, self.stream_counter, pos], n)
         self._pf_pos = pos
 
     __call__ = next_u32
