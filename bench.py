@@ -303,7 +303,7 @@ def headline_roofline(per_gen: dict, dom: str, pk: dict, sms: int, mhz: float, t
             "kernel": r.get("kernel"), "fractions": r["fractions"],
             "hbm": {"achieved": r["hbm_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
                     "frac": r["fractions"]["hbm"], "peak_source": pk["source"]},
-            "per_unit": r.get("per_unit"), "peak_source": peak_src,
+            "per_unit": r.get("per_unit"), "peak_source": peak_src, "hbm_free": r.get("hbm_free"),
             "algorithmic_bytes_per_launch": N_PER_GPU * 4,
             "pipe_work_source": "tools/sass_pipes.py on the loaded libcbrng_b200.so (hot-loop SASS)"}
 
@@ -370,6 +370,17 @@ def main() -> None:
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def timed(fn, reps=1):
+        fn()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / 1e3 / reps)
 
     def all_ranks_true(ok: bool) -> bool:
         if world == 1:
@@ -441,6 +452,22 @@ def main() -> None:
                       "digest": parity[a]}
         if rank == 0 and a in ref_d:
             per_gen[a]["matches_reference_fullsize"] = parity[a] == ref_d[a]
+    # HBM-free rate of the same kernels (libcbrng_ceiling.so: every store aimed at an
+    # L2-resident ring): achieved / HBM-free near 1 means the fill runs at the rate
+    # of its own instruction stream, whatever the HBM fraction says
+    try:
+        cl = _lib.ceiling_lib()
+        for a in ALGS[:3]:
+            def cfill(a=a):
+                _lib.check(cl.cbrng_uniform_f32(ALGS.index(a), 42, 0, 0, None, N_PER_GPU, out.data_ptr(), None, sptr),
+                           "ceiling fill")
+            c_ms = timed(cfill, reps=max(3, args.steps // 2)) * 1e3
+            per_gen[a]["roofline"]["hbm_free"] = {"ms": round(c_ms, 4),
+                                                  "frac": round(c_ms / per_gen[a]["ms"], 3),
+                                                  "what": "same kernel, stores into a 1 MB L2-resident ring "
+                                                          "(libcbrng_ceiling.so); frac = HBM-free ms / ms"}
+    except (OSError, RuntimeError) as exc:  # ceiling build absent: the product numbers stand alone
+        per_gen["philox"]["roofline"]["hbm_free_error"] = str(exc)[:200]
     dom = max(per_gen, key=lambda a: per_gen[a]["ms"])
     traffic = None
     prof = ROOT / "profiles" / "ncu_summary.json"
@@ -563,17 +590,6 @@ def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ran
     n1_file = ROOT / "tests" / "golden" / "gpu_n1_digests.json"  # tools/record_n1_digests.py
     n1 = json.loads(n1_file.read_text()) if (k == 1 and n1_file.exists()) else {}
 
-    def timed(fn, reps=1):
-        fn()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            fn()
-        e1.record(stream)
-        barrier()
-        return max_over_ranks(e0.elapsed_time(e1) / 1e3 / reps)
-
     def work_or_none(fn, *a):
         try:
             return fn(so, *a)
@@ -680,12 +696,28 @@ def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ran
     t_cu = timed(cu_bm)
     cr.cbrng_curand_destroy(g)
     pairs_s = BM_PAIRS / t / world
+    # HBM-free rate of the same Box-Muller kernel on one 2^29-pair launch (libcbrng_ceiling.so)
+    bm_free = None
+    try:
+        cl = _lib.ceiling_lib()
+        p29 = min(1 << 29, chunk)
+
+        def one(L):
+            _lib.check(L.cbrng_normal2_f64(0, 42, 0, 0, None, p29, z0.data_ptr(), z1.data_ptr(), None, sptr), "bm")
+
+        t_p, t_c = timed(lambda: one(lib), reps=5), timed(lambda: one(cl), reps=5)
+        bm_free = {"ms": round(t_c * 1e3, 4), "product_ms": round(t_p * 1e3, 4), "frac": round(t_c / t_p, 3),
+                   "what": "one 2^29-pair launch, same kernel with stores into a 1 MB L2-resident ring "
+                           "(libcbrng_ceiling.so); frac = HBM-free ms / product ms"}
+    except (OSError, RuntimeError) as exc:
+        bm_free = {"error": str(exc)[:200]}
     side["box_muller_f64"] = {
         "config": f"configs[3]: 2^34 normals (2^33 pairs) in total, long-stream layout, pair-range shards over "
                   f"{world} GPU(s)",
         "scaling": "strong",
         "seconds": round(t, 4), "gvalues_s": round(2 * BM_PAIRS / t / 1e9, 2),
-        "roofline": roofline_of(work_or_none(sass_pipes.fill_work, 0, 3), pairs_s, 16, pk, sms, mhz),
+        "roofline": {**roofline_of(work_or_none(sass_pipes.fill_work, 0, 3), pairs_s, 16, pk, sms, mhz),
+                     "hbm_free": bm_free},
         "curand_normal_double": {"seconds": round(t_cu, 4), "gvalues_s": round(2 * BM_PAIRS / t_cu / 1e9, 2),
                                  "api": "curandGenerateNormalDouble, CURAND_RNG_PSEUDO_PHILOX4_32_10"},
         "speedup_vs_curand": round(t_cu / t, 3),

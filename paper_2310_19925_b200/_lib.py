@@ -18,6 +18,7 @@ LIB_DIR = PKG / "_lib"
 LIB_PATH = LIB_DIR / "libcbrng_b200.so"
 TUNING_LIB_PATH = LIB_DIR / "libcbrng_b200_tuning.so"  # `make -C csrc tuning`: tools/ sweeps only
 CURAND_LIB_PATH = LIB_DIR / "libcbrng_curand_baseline.so"
+CEILING_LIB_PATH = LIB_DIR / "libcbrng_ceiling.so"  # measurement only: HBM-free fills (bench.py)
 HEADER = PKG.parent / "include" / "cbrng_b200.h"
 
 CBRNG_OK, CBRNG_EINVAL, CBRNG_EALG, CBRNG_ECUDA, CBRNG_EALIGN = 0, -1, -2, -3, -4
@@ -26,6 +27,7 @@ BROWNIAN_PER_STEP, BROWNIAN_FUSED = 0, 1
 _lock = threading.Lock()
 _lib = None
 _curand = None
+_ceiling = None
 
 u8p = C.POINTER(C.c_uint8)
 vp = C.c_void_p
@@ -162,6 +164,19 @@ def scalar(op: int, args, nout: int):
     out = np.empty(nout, np.uint32)
     check(lib().cbrng_scalar(op, buf, len(args), out.ctypes.data, nout), "cbrng_scalar")
     return out
+
+
+def ceiling_lib():
+    """The measurement-only build of the single-stream fills (-DCBRNG_CEILING=1): the same
+    kernels with every store aimed at an L2-resident ring, so bench.py can time the
+    HBM-free rate of the product's instruction stream. Never on a product path."""
+    global _ceiling
+    if _ceiling is None:
+        with _lock:
+            if _ceiling is None:
+                _ceiling = _bind(CEILING_LIB_PATH, {k: SIGNATURES[k] for k in
+                                                    ("cbrng_uniform_f32", "cbrng_normal2_f64", "cbrng_last_error")})
+    return _ceiling
 
 
 def last_error() -> str:

@@ -39,7 +39,11 @@ struct FillArgs {
 
 // CV: where the f32 map's shift / convert / scale run (u32_to_f32_cv).
 // BV: the lane's view of the Box-Muller tables (OUT_NORMAL only).
-// CV & 8 (tuning build, CBRNG_NOSTORE=1): HBM-free ceiling of the same kernel.
+#ifndef CBRNG_CEILING
+#define CBRNG_CEILING 0  // libcbrng_ceiling.so (bench.py): every single-stream fill stores into the ring
+#endif
+// CV & 8 (tuning build, CBRNG_NOSTORE=1) or CBRNG_CEILING (the measurement-only
+// libcbrng_ceiling.so that bench.py times live): HBM-free ceiling of the same kernel.
 // Unit u is stored at u mod 2^16 (a 1-2 MB ring that stays in L2), so the
 // instruction stream is the product's plus one LOP3 per store, and no output
 // reaches HBM. (A value-dependent store predicate instead splits the unrolled
@@ -47,7 +51,7 @@ struct FillArgs {
 template <int OUT, int CV = 0, class BV = BmView<>>
 __device__ __forceinline__ void store_unit(void *out0, void *out1, uint64_t u, uint4 w, uint32_t m24 = 0,
                                            const BV &bm = BV{}) {
-    if constexpr ((CV & 8) != 0) u &= 0xFFFFu;
+    if constexpr ((CV & 8) != 0 || CBRNG_CEILING) u &= 0xFFFFu;
     if constexpr (OUT == OUT_U32) {
         __stcs(reinterpret_cast<uint4 *>(out0) + u, w);
     } else if constexpr (OUT == OUT_F32) {
