@@ -590,6 +590,17 @@ def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ran
     n1_file = ROOT / "tests" / "golden" / "gpu_n1_digests.json"  # tools/record_n1_digests.py
     n1 = json.loads(n1_file.read_text()) if (k == 1 and n1_file.exists()) else {}
 
+    def timed(fn, reps=1):
+        fn()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / 1e3 / reps)
+
     def work_or_none(fn, *a):
         try:
             return fn(so, *a)
