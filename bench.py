@@ -466,6 +466,14 @@ def main() -> None:
                                                   "frac": round(c_ms / per_gen[a]["ms"], 3),
                                                   "what": "same kernel, stores into a 1 MB L2-resident ring "
                                                           "(libcbrng_ceiling.so); frac = HBM-free ms / ms"}
+        def cty():
+            _lib.check(cl.cbrng_prefix_uniform_f32(3, None, ty_lo, None, 0, TYCHE_STREAMS, TYCHE_WORDS, out.data_ptr(),
+                                                   sptr), "ceiling rows")
+        c_ms = timed(cty, reps=max(3, args.steps // 2)) * 1e3
+        per_gen["tyche"]["roofline"]["hbm_free"] = {"ms": round(c_ms, 4), "frac": round(c_ms / per_gen["tyche"]["ms"], 3),
+                                                    "what": "same kernel, rows of 2048-stream blocks into one 2 MB "
+                                                            "L2-resident ring (libcbrng_ceiling.so); frac = HBM-free "
+                                                            "ms / ms"}
     except (OSError, RuntimeError) as exc:  # ceiling build absent: the product numbers stand alone
         per_gen["philox"]["roofline"]["hbm_free_error"] = str(exc)[:200]
     dom = max(per_gen, key=lambda a: per_gen[a]["ms"])
@@ -753,11 +761,22 @@ def side_measurements(args, rank, world, dev, stream, lib, barrier, max_over_ran
     t_cu = timed(lambda: _lib.check(0 if cr.cbrng_curand_rows(lo, hi - lo, MS_WORDS, w.data_ptr(), sptr) == 0 else -3,
                                     "curand rows"), reps=3)
     words_s = MS_STREAMS * MS_WORDS / t / world
+    ms_free = None
+    try:  # HBM-free rate of the same rows kernel (libcbrng_ceiling.so: rows into one L2-resident ring)
+        cl = _lib.ceiling_lib()
+        t_c = timed(lambda: _lib.check(cl.cbrng_prefix_words(0, None, lo, None, 0, hi - lo, MS_WORDS, w.data_ptr(),
+                                                             sptr), "ceiling rows"), reps=3)
+        ms_free = {"seconds": round(t_c, 4), "frac": round(t_c / t, 3),
+                   "what": "same kernel, rows of 2048-stream blocks into one 2 MB L2-resident ring "
+                           "(libcbrng_ceiling.so); frac = HBM-free time / time"}
+    except (OSError, RuntimeError) as exc:
+        ms_free = {"error": str(exc)[:200]}
     side["multistream_words"] = {
         "config": f"configs[4]: 1e8 Philox streams x 256 words in total, stream-range shards over {world} GPU(s)",
         "scaling": "strong",
         "seconds": round(t, 4), "gwords_s": round(MS_STREAMS * MS_WORDS / t / 1e9, 2),
-        "roofline": roofline_of(work_or_none(sass_pipes.rows_work, 0, 0), words_s, 4, pk, sms, mhz),
+        "roofline": {**roofline_of(work_or_none(sass_pipes.rows_work, 0, 0), words_s, 4, pk, sms, mhz),
+                     "hbm_free": ms_free},
         "curand_rows": {"seconds": round(t_cu, 4), "gwords_s": round(MS_STREAMS * MS_WORDS / t_cu / 1e9, 2),
                         "api": "device API: curand_init(seed = stream, 0, 0) + curand4, one thread per stream"},
         "speedup_vs_curand": round(t_cu / t, 3),

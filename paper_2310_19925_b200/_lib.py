@@ -175,7 +175,8 @@ def ceiling_lib():
         with _lock:
             if _ceiling is None:
                 _ceiling = _bind(CEILING_LIB_PATH, {k: SIGNATURES[k] for k in
-                                                    ("cbrng_uniform_f32", "cbrng_normal2_f64", "cbrng_last_error")})
+                                                    ("cbrng_uniform_f32", "cbrng_normal2_f64", "cbrng_prefix_uniform_f32",
+                                                     "cbrng_prefix_words", "cbrng_last_error")})
     return _ceiling
 
 

@@ -39,9 +39,6 @@ struct FillArgs {
 
 // CV: where the f32 map's shift / convert / scale run (u32_to_f32_cv).
 // BV: the lane's view of the Box-Muller tables (OUT_NORMAL only).
-#ifndef CBRNG_CEILING
-#define CBRNG_CEILING 0  // libcbrng_ceiling.so (bench.py): every single-stream fill stores into the ring
-#endif
 // CV & 8 (tuning build, CBRNG_NOSTORE=1) or CBRNG_CEILING (the measurement-only
 // libcbrng_ceiling.so that bench.py times live): HBM-free ceiling of the same kernel.
 // Unit u is stored at u mod 2^16 (a 1-2 MB ring that stays in L2), so the

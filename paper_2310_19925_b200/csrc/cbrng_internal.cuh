@@ -24,6 +24,14 @@ namespace cbrng {
 
 constexpr bool TUNING = CBRNG_TUNING != 0;
 
+// CBRNG_CEILING=1 builds the measurement-only libcbrng_ceiling.so that bench.py
+// times beside the product: the single-stream fills and the multi-stream rows
+// store into a small ring that stays in L2, so the HBM-free rate of the same
+// instruction stream can be measured. Never set for the product library.
+#ifndef CBRNG_CEILING
+#define CBRNG_CEILING 0
+#endif
+
 // The value of environment knob `name` in [lo, hi] (tuning build), else dflt.
 int tuning_knob(const char *name, int dflt, int lo, int hi);
 

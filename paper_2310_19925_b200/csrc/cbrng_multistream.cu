@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(256, staged_min_blocks<ALG, VEC>()) staged_pre
         const bool valid = sid < a.n_streams;
         RowGen<ALG> gen(valid ? seed_of(a, sid) : 0, valid ? ctr_of(a, sid) : 0);
         // output word index of (row rrow + RPI k, chunk rc) in group g: at + k*rstride
-        uint64_t at = (s0 + rrow) * a.nwords + rc * 4;
+        // (CBRNG_CEILING: rows of 2048-stream blocks overwrite one L2-resident ring)
+        uint64_t at = ((CBRNG_CEILING ? (s0 & 2047u) : s0) + rrow) * a.nwords + rc * 4;
         const uint64_t rstride = (uint64_t)RPI * a.nwords;
         const uint32_t rows_left = a.n_streams - s0 < 32 ? (uint32_t)(a.n_streams - s0) : 32u;
         if constexpr (NW != 0 && VEC && CH == 4) {
