@@ -168,7 +168,8 @@ def host_threads() -> int:
 # ---------------------------------------------------------------------------
 
 def cpu_reference(steps: int, warmup: int, quick: bool) -> dict:
-    """configs[1] on the host: bounded sample per step."""
+    """configs[1] on the host: one step = the full per-GPU workload (4 x 2^30 f32 values;
+    Tyche 2^22 streams x 256), about 2-3 s on 16 cores (--quick: 2^22 values)."""
     import numpy as np
 
     from oracle import oracle as orc
@@ -176,7 +177,7 @@ def cpu_reference(steps: int, warmup: int, quick: bool) -> dict:
     orc.build()
     orc.set_num_threads(host_threads())
     threads = orc.num_threads()
-    sample = 1 << 25 if not quick else 1 << 22  # f32 values per generator per step
+    sample = N_PER_GPU if not quick else 1 << 22  # f32 values per generator per step
     ty_streams = sample // TYCHE_WORDS
     buf = np.empty(sample, np.float32)
 
@@ -206,7 +207,7 @@ def cpu_side_baselines(quick: bool) -> dict:
     orc.set_num_threads(host_threads())
     threads = orc.num_threads()
     out = {}
-    n, s = (200_000, 10) if quick else (2_000_000, 20)
+    n, s = (200_000, 10) if quick else (2_000_000, 100)  # ~10 s on 16 cores
     t = time.perf_counter()
     st = orc.brownian_init("philox", n, 0)
     orc.brownian_steps("philox", st, 1, s)
@@ -214,14 +215,14 @@ def cpu_side_baselines(quick: bool) -> dict:
     out["configs[2]"] = {"value": n * s / dt, "unit": "particle-steps/s", "cores": threads, "kind": "port",
                          "sample": f"init + {s} steps of {n} particles (oracle brownian_init/steps, OpenMP)",
                          "seconds": round(dt, 3)}
-    p = 1 << (20 if quick else 23)
+    p = 1 << (20 if quick else 28)
     t = time.perf_counter()
     orc.normal2("philox", 42, 0, p)
     dt = time.perf_counter() - t
     out["configs[3]"] = {"value": 2 * p / dt / 1e9, "unit": "Gvalues/s", "cores": threads, "kind": "port",
                          "sample": f"2^{p.bit_length() - 1} Box-Muller pairs (oracle words + libm, OpenMP)",
                          "seconds": round(dt, 3)}
-    r = 1 << (16 if quick else 20)
+    r = 1 << (16 if quick else 22)
     t = time.perf_counter()
     orc.prefix_words_arange("philox", 0, r, 0, MS_WORDS)
     dt = time.perf_counter() - t
@@ -253,7 +254,8 @@ def run_reference_arm(args) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": m["value"], "unit": "Gsamples/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["seconds"] / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": "configs[1] uniform_f32 x4 generators (bounded CPU sample)",
+            "config": {"workload": "configs[1] uniform_f32 x4 generators (the full per-GPU workload per step; "
+                                   "--quick: a 2^22-value sample)",
                        "sample": m["sample"]},
             "cpu_baseline": {"value": m["value"], "unit": "Gsamples/s", "cores": m["cores"], "kind": m["kind"],
                              "sample": m["sample"]},
@@ -561,7 +563,7 @@ def main() -> None:
 
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference(1, 1, args.quick)
+            cpu = cpu_reference(1 if args.quick else 4, 1, args.quick)  # ~10 s of host work
             cpu.pop("seconds", None)
             line["cpu_baseline"] = cpu
             if not (args.quick or args.no_side):
