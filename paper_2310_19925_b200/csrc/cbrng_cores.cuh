@@ -588,6 +588,9 @@ __device__ __forceinline__ uint32_t squares_rounds_234(uint64_t r, uint64_t y, u
 // An opaque zero in the constant bank: ptxas cannot fold it, and IADD3 takes
 // it as a c[] operand (no register). Tuning-build variants only (squares_x4_inc<true>).
 static __constant__ uint32_t c_zero = 0;
+// An opaque one, for addp<true> where the stream is set up on the device
+// (multi-stream Threefry rows): IMAD takes it as a c[] operand.
+static __constant__ uint32_t c_one = 1;
 
 // 64-bit a + b whose high half is a 3-input add against an opaque zero
 // (c_zero): ptxas then emits IADD3.X on the ALU pipe. Left as a

@@ -127,7 +127,10 @@ template <> struct RowGen<PHILOX> {
 template <> struct RowGen<THREEFRY> {
     ThreefryStream p;
     uint32_t b = 0;
-    __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) : p(threefry_stream_setup(seed, c)) {}
+    // p.one from the constant bank: set up on the device, a literal 1 would let
+    // ptxas fold the forced IMAD adds back into IADD3s on the ALU pipe, the pipe
+    // that bounds Threefry
+    __device__ __forceinline__ RowGen(uint64_t seed, uint32_t c) : p(threefry_stream_setup(seed, c)) { p.one = c_one; }
     __device__ __forceinline__ uint4 next4() { return threefry_stream_block<0, true, true>(p, b++); }
 };
 template <> struct RowGen<SQUARES> {
