@@ -1,0 +1,100 @@
+"""Randomised GPU parity (hypothesis) and library provenance.
+
+* Random (algorithm, seed, stream counter, word position, length) fills through the
+  public API against the oracle, bit for bit: the scalar transport (cbrng_scalar)
+  and the bulk fills (cbrng_words / cbrng_uniform_f32 / cbrng_uniform_f64), incl.
+  positions next to the 2^32-block / 2^32-counter wraps and mid-block resumes.
+* Random Box-Muller pairs against the oracle within the stated tolerance.
+* The process that ran them mapped the product library and never the
+  measurement-only builds (libcbrng_ceiling.so, the tuning build): the product
+  path has one implementation.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+from hypothesis import HealthCheck, given, settings
+from hypothesis import strategies as st
+
+pytestmark = pytest.mark.gpu
+
+M32, M64 = 0xFFFFFFFF, 0xFFFFFFFFFFFFFFFF
+ALGS = ["philox", "threefry", "squares"]
+SETTINGS = settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+
+
+@pytest.fixture(scope="module")
+def cb():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2310_19925_b200 as cb
+
+    return cb
+
+
+def _position(alg: str, pos: int) -> tuple[int, int]:
+    """(block_ctr, lane) of the oracle for stream word position `pos`."""
+    if alg == "squares":
+        return pos & M32, 0
+    return (pos >> 2) & M32, pos & 3
+
+
+positions = st.one_of(st.integers(0, 2**34 - 1), st.integers(2**34 - 70, 2**34 - 1),
+                      st.integers(2**32 - 70, 2**32 + 70))
+
+
+@SETTINGS
+@given(alg=st.sampled_from(ALGS), seed=st.integers(0, M64), sc=st.integers(0, M32), pos=positions,
+       n=st.integers(0, 700))
+def test_scalar_stream_words(cb, oracle, alg, seed, sc, pos, n):
+    from paper_2310_19925_b200 import _lib
+
+    got = _lib.scalar(_lib.SCALAR_STREAM_WORDS, [ALGS.index(alg), seed, sc, pos], n)
+    blk, lane = _position(alg, pos)
+    ref = oracle.stream_words(alg, seed, sc, n, block_ctr=blk, lane=lane) if n else np.empty(0, np.uint32)
+    assert np.array_equal(got, ref)
+
+
+@SETTINGS
+@given(alg=st.sampled_from(ALGS), seed=st.integers(0, M64), sc=st.integers(0, M32), pos=positions,
+       n=st.integers(1, 5000), kind=st.sampled_from(["u32", "f32", "f64"]))
+def test_bulk_fill_from_any_position(cb, oracle, alg, seed, sc, pos, n, kind):
+    g = cb.make_generator(alg, seed, sc)
+    g._advance(pos)
+    blk, lane = _position(alg, pos)
+    if kind == "u32":
+        got = g.words(n).cpu().numpy()
+        ref = oracle.stream_words(alg, seed, sc, n, block_ctr=blk, lane=lane)
+    elif kind == "f32":
+        got = cb.uniform_f32_array(g, n).cpu().numpy()
+        ref = oracle.words_to_f32(oracle.stream_words(alg, seed, sc, n, block_ctr=blk, lane=lane))
+    else:
+        got = cb.uniform_f64_array(g, n).cpu().numpy()
+        ref = oracle.words_to_f64(oracle.stream_words(alg, seed, sc, 2 * n, block_ctr=blk, lane=lane))
+    assert np.array_equal(got, ref)
+    # the generator advanced exactly as n scalar draws would have
+    g2 = cb.make_generator(alg, seed, sc)
+    g2._advance(pos + (2 * n if kind == "f64" else n))
+    assert g.state_bytes() == g2.state_bytes()
+
+
+@SETTINGS
+@given(seed=st.integers(0, M64), sc=st.integers(0, M32), n=st.integers(1, 3000))
+def test_box_muller_random_streams(cb, oracle, seed, sc, n):
+    z0, z1 = cb.normal2_array(cb.make_generator("philox", seed, sc), n)
+    r0, r1 = oracle.normal2("philox", seed, sc, n)
+    for got, ref in ((z0.cpu().numpy(), r0), (z1.cpu().numpy(), r1)):
+        assert np.all(np.abs(got - ref) <= 4 * np.spacing(np.maximum(np.abs(ref), 1.0)))
+
+
+def test_only_the_product_library_is_mapped(cb):
+    """After the calls above: the product .so is mapped, the measurement-only builds are not."""
+    cb.uniform_f32_array(cb.make_generator("philox", 1, 2), 1000)
+    cb.philox_block((1, 2), (3, 4, 5, 6))
+    maps = open("/proc/self/maps").read()
+    assert "libcbrng_b200.so" in maps
+    assert "libcbrng_ceiling.so" not in maps
+    assert "libcbrng_b200_tuning.so" not in maps
