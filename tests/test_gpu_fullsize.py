@@ -91,7 +91,7 @@ def test_cfg3_every_value_within_tolerance(cb, oracle):
     """All 2^33 pairs of the long-stream layout (pair i: stream (42, i div 2^32),
     block i mod 2^32), compared on the host against the reference formula in
     chunks of 2^28 pairs. Bounds: 4 ulp(max(|z|, 1)) and 8 ulps of z per value
-    (round 2 measured: 3 and 5)."""
+    (r2z kernel measured: 3 and 4)."""
     import torch
     from paper_2310_19925_b200 import sharding
 

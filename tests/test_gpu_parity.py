@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 M32 = 0xFFFFFFFF
 BM_ULP = 4  # Box-Muller tolerance, in ulp(max(|z|, 1))
-BM_REL_ULP = 8  # and in ulps of z itself (observed: 5 over all 2^34 values of configs[3])
+BM_REL_ULP = 8  # and in ulps of z itself (observed: 4 over all 2^34 values of configs[3], r2z kernel)
 
 
 def sha(a) -> str:
