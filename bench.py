@@ -454,6 +454,19 @@ def main() -> None:
                       "digest": parity[a]}
         if rank == 0 and a in ref_d:
             per_gen[a]["matches_reference_fullsize"] = parity[a] == ref_d[a]
+    # the Tyche layout (2^22 streams x 256, rows) reported for all four
+    for a in ALGS[:3]:
+        def rows(a=a):
+            _lib.check(lib.cbrng_prefix_uniform_f32(ALGS.index(a), None, ty_lo, None, 0, TYCHE_STREAMS, TYCHE_WORDS,
+                                                    out.data_ptr(), sptr), "rows")
+        r_ms = timed(rows, reps=max(3, args.steps // 2)) * 1e3
+        per_gen[a]["rows_layout"] = {"ms": round(r_ms, 4), "gsamples_s": round(N_PER_GPU / r_ms / 1e6, 2),
+                                     "hbm_gbs": round(N_PER_GPU * 4 / r_ms / 1e6, 1),
+                                     "what": "uniform f32, 2^22 streams (seeds r 2^22 + i, ctr 0) x 256 values, "
+                                             "row-major: the Tyche layout of configs[1] (bulk.prefix_uniform_f32)"}
+    per_gen["tyche"]["rows_layout"] = {"ms": per_gen["tyche"]["ms"], "gsamples_s": per_gen["tyche"]["gsamples_s"],
+                                       "what": "the headline Tyche fill itself"}
+
     # HBM-free rate of the same kernels (libcbrng_ceiling.so: every store aimed at an
     # L2-resident ring): achieved / HBM-free near 1 means the fill runs at the rate
     # of its own instruction stream, whatever the HBM fraction says
