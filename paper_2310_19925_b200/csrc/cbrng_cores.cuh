@@ -623,7 +623,7 @@ __device__ __forceinline__ uint64_t add64_3(uint64_t a, uint64_t b, uint64_t c) 
 // z_k = x_k + key = x_{k+1}. k2x2 = 2 key^2, k2x4 = 4 key^2; x4_out <- x_4.
 // ALUC (tuning build): every carry add forced onto the ALU pipe (add64_alu /
 // add64_3: E_1, E_2 folded into 3-input adds). It removes 9 % of the
-// FMA-heavy slots (IMAD.X) and measured 2 % slower (profiles/r2d_tune.md).
+// FMA-heavy slots (IMAD.X) and measured 2 % slower (profiles/r2k_tune.md).
 template <bool ALUC = false>
 __device__ __forceinline__ uint4 squares_x4_inc(uint64_t x0, uint64_t e0, uint64_t key, uint64_t k2x2, uint64_t k2x4,
                                                 uint64_t *x4_out = nullptr) {

@@ -300,9 +300,11 @@ constexpr int fill_ilp_default() {
 // Default code variants (B200 sweeps, profiles/r1r_tune.md): Threefry V (see
 // block_at) and the f32 conversion placement CV (see u32_to_f32_cv) per
 // generator. Tuning build: CBRNG_FILL_ILP=8|12|16, CBRNG_TF_VARIANT=0..8,
-// CBRNG_CVT=0..5, CBRNG_BM_MINB=0|8, CBRNG_SQ_INC=0|1, CBRNG_MULTI=0|1.
+// CBRNG_CVT=0..5, CBRNG_SQ_INC=0..2, CBRNG_SQ_MINB=0|6, CBRNG_MULTI=0|1,
+// CBRNG_BM_LAYOUT=0..12, CBRNG_BM_SPLIT=0|1, CBRNG_BM_GRID, CBRNG_NOSTORE=0|1.
+
 // Box-Muller fill shape (normal_fill_kernel): ILP pairs per thread, LC / SC
-// table copies, NT threads per CTA, MB CTAs per SM (profiles/r2e_tune.md).
+// table copies, NT threads per CTA, MB CTAs per SM (profiles/r2d_tune.md).
 constexpr int BM_ILP = 8, BM_LC = 8, BM_SC = 2, BM_NT = 1024, BM_MB = 2, BM_LAYOUT_DEFAULT = 5;
 
 template <int ALG, bool SKIP, int V, int ILP, int LC, int SC, int NT, int MB, bool PIPE = false>
@@ -329,7 +331,7 @@ static int launch_normal(const FillArgs<ALG> &a, cudaStream_t st) {
 
 template <int ALG> constexpr int cv_default() { return 4; }  // all three fills: SHF + I2F (XU) + FMUL
 
-// Tuning build: the Box-Muller fill shapes of CBRNG_BM_LAYOUT (profiles/r2e_tune.md).
+// Tuning build: the Box-Muller fill shapes of CBRNG_BM_LAYOUT (profiles/r2d_tune.md).
 template <int ALG, bool SKIP, int VS>
 static int launch_normal_layout(const FillArgs<ALG> &a, cudaStream_t st, int lay) {
     switch (lay) {
@@ -375,7 +377,7 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
         return launch_fill_ilp<ALG, OUT, SKIP, I0, V, CV>(a, st);
     } else if constexpr (OUT == OUT_NORMAL) {
         if constexpr (TUNING && ALG == PHILOX && !SKIP) {
-            // CBRNG_BM_SPLIT=1: Philox mulhilo as IMAD.HI + IMAD (V 1), measured 10 % slower (r2g)
+            // CBRNG_BM_SPLIT=1: Philox mulhilo as IMAD.HI + IMAD (V 1), measured 10 % slower (profiles/r2d_tune.md)
             static const int split = tuning_knob("CBRNG_BM_SPLIT", 0, 0, 1);
             static const int lay = tuning_knob("CBRNG_BM_LAYOUT", BM_LAYOUT_DEFAULT, 0, 12);
             return split ? launch_normal_layout<ALG, SKIP, 1>(a, st, lay) : launch_normal_layout<ALG, SKIP, V>(a, st, lay);
