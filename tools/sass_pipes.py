@@ -173,7 +173,16 @@ def rows_work(so: str, alg: int, out: int) -> dict:
     """Per word of 256-word rows (staged_prefix_kernel<..., 256>): the group loop
     (16 words per thread) plus, for Tyche, the per-row warm-up over 256 words."""
     name, ins = find(so, rf"staged_prefix_kernel<{alg}, {out}, true, \d+, 4, 256>")
-    lo, hi = hot_loop(ins, must="STG")
+    # the kernel has two group loops: the generic one (per-row store predicates: an
+    # ISETP per row slot) and the full-warp 256-word-row path that every launch of
+    # 2^k x 32 rows takes (one ISETP, the loop test); time goes to the second
+    cands = [l for l in innermost(loops(ins))
+             if any(op.startswith("STG") for a, op, _ in ins if l[0] <= a <= l[1])
+             and any(op.startswith("STS") for a, op, _ in ins if l[0] <= a <= l[1])]
+    if not cands:
+        raise LookupError("no staged group loop")
+    lo, hi = min(cands, key=lambda l: (sum(1 for a, op, _ in ins if l[0] <= a <= l[1] and op.startswith("ISETP")),
+                                       -(l[1] - l[0])))
     w = pipes(mix(ins, lo, hi), 16)
     res = {"kernel": name, "unit": "word", "loop": [hex(lo), hex(hi)]}
     if alg == 3:
