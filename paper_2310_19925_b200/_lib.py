@@ -150,6 +150,22 @@ SCALAR_MAX_WORDS = 1 << 18
 _scalar_tls = threading.local()
 
 
+def scalar_small(op: int, args, nout: int) -> list:
+    """cbrng_scalar for the block functions (ops 0-5, at most 4 result words): the
+    same round trip into thread-local ctypes buffers, the words as a list."""
+    tls = _scalar_tls
+    buf = getattr(tls, "args", None)
+    if buf is None:
+        buf = tls.args = (C.c_uint64 * 16)()
+    out = getattr(tls, "out", None)
+    if out is None:
+        out = tls.out = (C.c_uint32 * 4)()
+    for i, a in enumerate(args):
+        buf[i] = a & 0xFFFFFFFFFFFFFFFF
+    check(lib().cbrng_scalar(op, buf, len(args), out, nout), "cbrng_scalar")
+    return out[:nout]
+
+
 def scalar(op: int, args, nout: int):
     """One synchronous scalar round trip through cbrng_scalar (host args, host
     result): a uint32 numpy array of nout words. Used by the reference's scalar

@@ -66,9 +66,10 @@ int resident_blocks(const void *kernel, int block, size_t smem) {
 }
 
 // Scalar transport (cbrng_scalar): per device, one mapped pinned host buffer
-// (inputs at offset 0, outputs at SCALAR_OUT_OFF) and one non-blocking stream.
-// The kernels read their few inputs and write their outputs straight through
-// the mapping, so a call is one launch and one stream synchronisation.
+// (outputs at SCALAR_OUT_OFF) and one non-blocking stream. The block functions
+// take their arguments by value (scalar_kernel) and every kernel writes its
+// output straight through the mapping, so a call is one launch and one stream
+// synchronisation, with nothing read over PCIe.
 constexpr size_t SCALAR_OUT_OFF = 4096, SCALAR_OUT_WORDS = 1u << 18;
 struct ScalarCtx {
     std::mutex mu;
@@ -133,37 +134,21 @@ int cbrng_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, ui
     ScalarCtx *c = scalar_ctx(rc);
     if (!c) return rc;
     std::lock_guard<std::mutex> g(c->mu);
-    uint32_t *in32 = reinterpret_cast<uint32_t *>(c->host);
-    uint64_t *in64 = reinterpret_cast<uint64_t *>(c->host);
-    const uint32_t *din32 = reinterpret_cast<const uint32_t *>(c->dev);
-    const uint64_t *din64 = reinterpret_cast<const uint64_t *>(c->dev);
     uint32_t *hout = reinterpret_cast<uint32_t *>(c->host + SCALAR_OUT_OFF);
     uint32_t *dout = reinterpret_cast<uint32_t *>(c->dev + SCALAR_OUT_OFF);
     void *st = c->st;
     switch (op) {
-        case CBRNG_SCALAR_PHILOX_BLOCK:  // ctr[4], key[2] (u32 each)
-            for (int i = 0; i < 6; i++) in32[i] = (uint32_t)args[i];
-            rc = cbrng_philox4x32(din32, din32 + 4, 1, dout, st);
-            break;
+        case CBRNG_SCALAR_PHILOX_BLOCK:    // ctr[4], key[2]
         case CBRNG_SCALAR_THREEFRY_BLOCK:  // ctr[4], key[4], rounds
-            for (int i = 0; i < 8; i++) in32[i] = (uint32_t)args[i];
-            rc = cbrng_threefry4x32(din32, din32 + 4, (int)args[8], 1, dout, st);
-            break;
-        case CBRNG_SCALAR_SQUARES_KEY:  // seed -> key (lo, hi)
-            in64[0] = args[0];
-            rc = cbrng_squares_keys(din64, 1, reinterpret_cast<uint64_t *>(dout), st);
-            break;
-        case CBRNG_SCALAR_SQUARES_ROUND:  // key, ctr
-            in64[0] = args[1];
-            in64[1] = args[0];
-            rc = cbrng_squares32(din64, din64 + 1, 1, dout, st);
-            break;
-        case CBRNG_SCALAR_TYCHE_INIT:  // seed, stream counter -> state[4]
-            rc = cbrng_tyche_init(nullptr, args[0], nullptr, (uint32_t)args[1], 1, dout, st);
-            break;
-        case CBRNG_SCALAR_TYCHE_MIX:  // state[4], rounds -> state[4]
-            for (int i = 0; i < 4; i++) hout[i] = (uint32_t)args[i];
-            rc = args[4] ? cbrng_tyche_mix(dout, 1, (uint32_t)args[4], st) : CBRNG_OK;
+        case CBRNG_SCALAR_SQUARES_KEY:     // seed -> key (lo, hi)
+        case CBRNG_SCALAR_SQUARES_ROUND:   // key, ctr
+        case CBRNG_SCALAR_TYCHE_INIT:      // seed, stream counter -> state[4]
+        case CBRNG_SCALAR_TYCHE_MIX:       // state[4], rounds -> state[4]
+            if (op == CBRNG_SCALAR_THREEFRY_BLOCK && args[8] > (1u << 20)) {  // < 0 or absurd: one thread would spin
+                set_error("rounds must be in [0, 2^20]");
+                return CBRNG_EINVAL;
+            }
+            rc = launch_scalar(op, args, nargs, dout, c->st);
             break;
         case CBRNG_SCALAR_STREAM_WORDS:  // alg, seed, stream counter, word position -> nout words
             if (args[0] > 2) {

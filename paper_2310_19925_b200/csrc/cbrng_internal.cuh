@@ -87,6 +87,9 @@ inline int check_cuda(cudaError_t e, const char *what) {
 // CTAs (cached per kernel x device), capped by the amount of work.
 int resident_blocks(const void *kernel, int block, size_t smem);
 
+// cbrng_scalar ops 0-5: one thread, arguments by value (cbrng_multistream.cu).
+int launch_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, cudaStream_t st);
+
 // Grid policy for the streaming kernels: k x the resident grid (grid-stride),
 // k = 8 (tuning build: CBRNG_GRID_MULT = k >= 1, or 0 = one tile per warp). The
 // write-only probe (tools/probe_store.py) reaches 6.2 TB/s from a resident

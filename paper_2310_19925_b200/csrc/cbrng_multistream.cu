@@ -549,6 +549,56 @@ __global__ void tyche_init_kernel(const uint64_t *seeds, uint64_t seed_base, con
     }
 }
 
+// One scalar block function with its arguments by value (cbrng_scalar ops 0-5):
+// the result goes straight into the caller's mapped pinned buffer, so a call
+// costs one launch and one synchronisation and reads nothing over PCIe.
+struct ScalarArgs {
+    uint64_t a[9];
+};
+
+__global__ void scalar_kernel(int op, const __grid_constant__ ScalarArgs s, uint32_t *out) {
+    const uint64_t *a = s.a;
+    switch (op) {
+        case 0: {  // philox_block: ctr0..3, key0..1
+            const uint4 r = philox_block(make_uint4((uint32_t)a[0], (uint32_t)a[1], (uint32_t)a[2], (uint32_t)a[3]),
+                                         (uint32_t)a[4], (uint32_t)a[5]);
+            out[0] = r.x; out[1] = r.y; out[2] = r.z; out[3] = r.w;
+            break;
+        }
+        case 1: {  // threefry_block: ctr0..3, key0..3, rounds
+            const uint4 c = make_uint4((uint32_t)a[0], (uint32_t)a[1], (uint32_t)a[2], (uint32_t)a[3]);
+            uint32_t k[4] = {(uint32_t)a[4], (uint32_t)a[5], (uint32_t)a[6], (uint32_t)a[7]};
+            const uint4 r = threefry_block_rounds(c, k, (int)a[8]);
+            out[0] = r.x; out[1] = r.y; out[2] = r.z; out[3] = r.w;
+            break;
+        }
+        case 2: {  // squares_key: seed -> (lo, hi)
+            const uint64_t k = squares_key(a[0]);
+            out[0] = (uint32_t)k; out[1] = (uint32_t)(k >> 32);
+            break;
+        }
+        case 3: out[0] = squares_round(a[0], a[1]); break;  // key, ctr
+        case 4: {  // tyche_init: seed, stream counter
+            const uint4 t = tyche_init(a[0], (uint32_t)a[1]);
+            out[0] = t.x; out[1] = t.y; out[2] = t.z; out[3] = t.w;
+            break;
+        }
+        default: {  // tyche_mix x rounds: state0..3, rounds
+            uint32_t w = (uint32_t)a[0], x = (uint32_t)a[1], y = (uint32_t)a[2], z = (uint32_t)a[3];
+            for (uint64_t r = 0; r < a[4]; r++) tyche_mix(w, x, y, z);
+            out[0] = w; out[1] = x; out[2] = y; out[3] = z;
+            break;
+        }
+    }
+}
+
+int launch_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, cudaStream_t st) {
+    ScalarArgs s = {};
+    for (uint32_t i = 0; i < nargs && i < 9; i++) s.a[i] = args[i];
+    scalar_kernel<<<1, 1, 0, st>>>(op, s, out);
+    return check_launch("scalar_kernel");
+}
+
 __global__ void philox_block_lanes_kernel(const uint64_t *seeds, const uint64_t *scs, uint64_t block_ctr, uint64_t n,
                                           uint32_t *out) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {

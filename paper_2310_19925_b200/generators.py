@@ -97,7 +97,7 @@ def rotl32(x: int, r: int) -> int:
 def philox_block(key, ctr) -> Block:
     from . import _lib
 
-    return Block(*(int(w) for w in _lib.scalar(_lib.SCALAR_PHILOX_BLOCK, [*ctr, *key], 4)))
+    return Block(*_lib.scalar_small(_lib.SCALAR_PHILOX_BLOCK, (*ctr, *key), 4))
 
 
 def threefry_block(key, ctr, rounds: int = THREEFRY_ROUNDS) -> Block:
@@ -105,32 +105,32 @@ def threefry_block(key, ctr, rounds: int = THREEFRY_ROUNDS) -> Block:
 
     if rounds < 0:
         raise ValueError("rounds must be >= 0")
-    return Block(*(int(w) for w in _lib.scalar(_lib.SCALAR_THREEFRY_BLOCK, [*ctr, *key, rounds], 4)))
+    return Block(*_lib.scalar_small(_lib.SCALAR_THREEFRY_BLOCK, (*ctr, *key, rounds), 4))
 
 
 def squares_key(seed: int) -> int:
     from . import _lib
 
-    lo, hi = _lib.scalar(_lib.SCALAR_SQUARES_KEY, [seed & MASK64], 2)
-    return (int(hi) << 32) | int(lo)
+    lo, hi = _lib.scalar_small(_lib.SCALAR_SQUARES_KEY, (seed,), 2)
+    return (hi << 32) | lo
 
 
 def squares_round(seed_key: int, counter: int) -> int:
     from . import _lib
 
-    return int(_lib.scalar(_lib.SCALAR_SQUARES_ROUND, [seed_key & MASK64, counter & MASK64], 1)[0])
+    return _lib.scalar_small(_lib.SCALAR_SQUARES_ROUND, (seed_key, counter), 1)[0]
 
 
 def tyche_mix(state) -> tuple[int, int, int, int]:
     from . import _lib
 
-    return tuple(int(w) for w in _lib.scalar(_lib.SCALAR_TYCHE_MIX, [*(w & MASK32 for w in state), 1], 4))
+    return tuple(_lib.scalar_small(_lib.SCALAR_TYCHE_MIX, (*(w & MASK32 for w in state), 1), 4))
 
 
 def tyche_init(seed: int, stream_counter: int) -> tuple[int, int, int, int]:
     from . import _lib
 
-    return tuple(int(w) for w in _lib.scalar(_lib.SCALAR_TYCHE_INIT, [seed & MASK64, stream_counter & MASK32], 4))
+    return tuple(_lib.scalar_small(_lib.SCALAR_TYCHE_INIT, (seed, stream_counter & MASK32), 4))
 
 
 def tyche_next(state) -> tuple[int, tuple[int, int, int, int]]:
