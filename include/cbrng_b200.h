@@ -158,11 +158,14 @@ int cbrng_tyche_init(const uint64_t *seeds, uint64_t seed_base, const uint32_t *
  *   TYCHE_INIT     seed, stream_ctr                      -> state[4]  (generators.py:190-218)
  *   TYCHE_MIX      state0..3, rounds                     -> state[4]  (generators.py:201-210)
  *   STREAM_WORDS   alg (0-2), seed, stream_ctr, word_pos -> nout words (<= 2^18) of cbrng_words
- *   TYCHE_WORDS    state0..3                             -> nout-4 words, then the state after them */
+ *   TYCHE_WORDS    state0..3                             -> nout-4 words, then the state after them
+ *   TYCHE_SEED_WORDS seed, stream_ctr                    -> the state after tyche_init (4), nout-8 words,
+ *                                                           then the state after them (a fresh stream's
+ *                                                           first window in one round trip) */
 enum {
     CBRNG_SCALAR_PHILOX_BLOCK = 0, CBRNG_SCALAR_THREEFRY_BLOCK = 1, CBRNG_SCALAR_SQUARES_KEY = 2,
     CBRNG_SCALAR_SQUARES_ROUND = 3, CBRNG_SCALAR_TYCHE_INIT = 4, CBRNG_SCALAR_TYCHE_MIX = 5,
-    CBRNG_SCALAR_STREAM_WORDS = 6, CBRNG_SCALAR_TYCHE_WORDS = 7
+    CBRNG_SCALAR_STREAM_WORDS = 6, CBRNG_SCALAR_TYCHE_WORDS = 7, CBRNG_SCALAR_TYCHE_SEED_WORDS = 8
 };
 int cbrng_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, uint64_t nout);
 

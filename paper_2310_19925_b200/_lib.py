@@ -145,7 +145,7 @@ def curand_lib():
 
 # cbrng_scalar ops (include/cbrng_b200.h)
 (SCALAR_PHILOX_BLOCK, SCALAR_THREEFRY_BLOCK, SCALAR_SQUARES_KEY, SCALAR_SQUARES_ROUND, SCALAR_TYCHE_INIT,
- SCALAR_TYCHE_MIX, SCALAR_STREAM_WORDS, SCALAR_TYCHE_WORDS) = range(8)
+ SCALAR_TYCHE_MIX, SCALAR_STREAM_WORDS, SCALAR_TYCHE_WORDS, SCALAR_TYCHE_SEED_WORDS) = range(9)
 SCALAR_MAX_WORDS = 1 << 18
 _scalar_tls = threading.local()
 

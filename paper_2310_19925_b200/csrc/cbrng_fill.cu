@@ -251,6 +251,24 @@ __global__ void tyche_stream_kernel(uint4 s, uint64_t n, void *out0, void *out1,
     }
 }
 
+// A fresh Tyche stream's first words in one launch (cbrng_scalar op
+// TYCHE_SEED_WORDS): out = [state after tyche_init (4), n words, final state (4)].
+__global__ void tyche_seed_words_kernel(uint64_t seed, uint32_t sc, uint64_t n, uint32_t *out, uint32_t z) {
+    const uint4 s = tyche_init(seed, sc);
+    out[0] = s.x; out[1] = s.y; out[2] = s.z; out[3] = s.w;
+    uint32_t a = s.x, b = s.y, c = s.z, d = s.w;
+    for (uint64_t i = 0; i < n; i++) {
+        tyche_mix_alu(a, b, c, d, z);
+        out[4 + i] = b;
+    }
+    out[4 + n] = a; out[5 + n] = b; out[6 + n] = c; out[7 + n] = d;
+}
+
+int launch_tyche_seed_words(uint64_t seed, uint32_t sc, uint64_t n, uint32_t *out, cudaStream_t st) {
+    tyche_seed_words_kernel<<<1, 1, 0, st>>>(seed, sc, n, out, 0u);
+    return check_launch("tyche_seed_words_kernel");
+}
+
 // Box-Muller over caller-supplied words (4 per pair): the transform of
 // normal2 / normal2_array applied to any word source (the reference tests it
 // with scripted generators, test_distributions.py:29-40, 178-186).

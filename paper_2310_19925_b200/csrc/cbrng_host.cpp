@@ -116,9 +116,9 @@ extern "C" {
 int cbrng_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, uint64_t nout) {
     using namespace cbrng;
     clear_error();
-    static const uint32_t NARGS[8] = {6, 9, 1, 2, 2, 5, 4, 4};
+    static const uint32_t NARGS[9] = {6, 9, 1, 2, 2, 5, 4, 4, 2};
     static const uint64_t NOUT[6] = {4, 4, 2, 1, 4, 4};
-    if (op < 0 || op > 7) {
+    if (op < 0 || op > 8) {
         set_error("unknown scalar op %d", op);
         return CBRNG_EINVAL;
     }
@@ -126,7 +126,8 @@ int cbrng_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, ui
         set_error("scalar op %d: expects %u args and an output buffer", op, NARGS[op]);
         return CBRNG_EINVAL;
     }
-    if (op < 6 ? nout != NOUT[op] : (op == 6 ? nout > SCALAR_OUT_WORDS : (nout < 4 || nout > SCALAR_OUT_WORDS))) {
+    const uint64_t min_out = op == 7 ? 4 : (op == 8 ? 8 : 0);
+    if (op < 6 ? nout != NOUT[op] : (nout < min_out || nout > SCALAR_OUT_WORDS)) {
         set_error("scalar op %d: bad output length %llu", op, (unsigned long long)nout);
         return CBRNG_EINVAL;
     }
@@ -157,6 +158,9 @@ int cbrng_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, ui
             }
             rc = nout ? cbrng_words((int)args[0], args[1], (uint32_t)args[2], args[3], nullptr, nout, dout, nullptr, st)
                       : CBRNG_OK;
+            break;
+        case CBRNG_SCALAR_TYCHE_SEED_WORDS:  // seed, stream counter -> init state, nout - 8 words, final state
+            rc = launch_tyche_seed_words(args[0], (uint32_t)args[1], nout - 8, dout, c->st);
             break;
         default: {  // CBRNG_SCALAR_TYCHE_WORDS: state[4] -> nout - 4 words, then the state after them
             uint32_t s4[4];

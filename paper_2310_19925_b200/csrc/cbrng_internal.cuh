@@ -89,6 +89,8 @@ int resident_blocks(const void *kernel, int block, size_t smem);
 
 // cbrng_scalar ops 0-5: one thread, arguments by value (cbrng_multistream.cu).
 int launch_scalar(int op, const uint64_t *args, uint32_t nargs, uint32_t *out, cudaStream_t st);
+// cbrng_scalar op TYCHE_SEED_WORDS (cbrng_fill.cu).
+int launch_tyche_seed_words(uint64_t seed, uint32_t sc, uint64_t n, uint32_t *out, cudaStream_t st);
 
 // Grid policy for the streaming kernels: k x the resident grid (grid-stride),
 // k = 8 (tuning build: CBRNG_GRID_MULT = k >= 1, or 0 = one tile per warp). The

@@ -254,15 +254,19 @@ class Generator:
     def next_u32(self) -> int:
         """Next 32-bit word of the stream."""
         if self.algorithm is Algorithm.TYCHE:
-            self._tyche_end_state()
-            if self._ty_pending.size == 0:
+            if self._ty_state is None or self._ty_pending.size == 0:
                 from . import _lib
 
                 n = self._pf_n
                 self._pf_n = min(self._pf_n * 2, _PF_MAX)
-                self._ty_base = self._ty_state
-                r = _lib.scalar(_lib.SCALAR_TYCHE_WORDS, self._ty_state, n + 4)
-                self._ty_pending, self._ty_state = r[:n], tuple(int(w) for w in r[n:])
+                if self._ty_state is None:  # fresh stream: init + first window in one round trip
+                    r = _lib.scalar(_lib.SCALAR_TYCHE_SEED_WORDS, [self.seed, self.stream_counter], n + 8)
+                    self._ty_base = tuple(r[:4].tolist())
+                    self._ty_pending, self._ty_state = r[4:4 + n], tuple(r[4 + n:].tolist())
+                else:
+                    self._ty_base = self._ty_state
+                    r = _lib.scalar(_lib.SCALAR_TYCHE_WORDS, self._ty_state, n + 4)
+                    self._ty_pending, self._ty_state = r[:n], tuple(r[n:].tolist())
                 self._ty_win = n
             w = int(self._ty_pending[0])
             self._ty_pending = self._ty_pending[1:]

@@ -82,11 +82,23 @@ def test_tyche_words(cb, oracle, n):
     assert np.array_equal(r[:n], ref) and tuple(int(v) for v in r[n:]) == tuple(fin)
 
 
+@pytest.mark.parametrize("n", [0, 1, 63, 64, 1000])
+def test_tyche_seed_words(cb, oracle, n):
+    """A fresh Tyche stream's init state, first n words and final state in one call."""
+    from paper_2310_19925_b200 import _lib
+
+    r = _lib.scalar(_lib.SCALAR_TYCHE_SEED_WORDS, [0x0123456789ABCDEF, 77], n + 8)
+    s = oracle.tyche_init(0x0123456789ABCDEF, 77)
+    ref, fin = oracle.stream_words("tyche", 0, 0, n, tyche_state=s) if n else (np.empty(0, np.uint32), s)
+    assert tuple(int(v) for v in r[:4]) == tuple(s)
+    assert np.array_equal(r[4:4 + n], ref) and tuple(int(v) for v in r[4 + n:]) == tuple(fin)
+
+
 def test_errors(cb):
     from paper_2310_19925_b200 import _lib
 
     with pytest.raises(ValueError):
-        _lib.scalar(8, [], 1)  # unknown op
+        _lib.scalar(9, [], 1)  # unknown op
     with pytest.raises(ValueError):
         _lib.scalar(_lib.SCALAR_PHILOX_BLOCK, [1, 2, 3], 4)  # wrong arity
     with pytest.raises(ValueError):
