@@ -143,33 +143,39 @@ __device__ __forceinline__ void philox_round_d(uint32_t &c0, uint32_t &c1, uint3
     c3 = l0;
 }
 
-// SPLIT: mulhilo as IMAD.HI + IMAD (mulhilo_c), for kernels that mix in FP64.
-template <bool SPLIT = false>
+// SPLIT: bit r set = round r's mulhilos as IMAD.HI + IMAD (mulhilo_c), for
+// kernels that mix in FP64 (1 = every round).
+template <int SPLIT = 0>
 __device__ __forceinline__ uint4 philox_stream_block(const PhiloxStream& p, uint32_t bc) {
+    constexpr int M = SPLIT == 1 ? 0x3FF : SPLIT;
     uint32_t c0, c1, c2, c3, h, l;
     // round 0
     c0 = bc ^ p.k0_0;
     // round 1
-    mulhilo_c<PHILOX_M0, SPLIT>(c0, h, l);
+    mulhilo_c<PHILOX_M0, (M >> 1) & 1>(c0, h, l);
     c2 = h ^ p.a1;
     c3 = l;
     // round 2
-    mulhilo_c<PHILOX_M1, SPLIT>(c2, h, l);
+    mulhilo_c<PHILOX_M1, (M >> 2) & 1>(c2, h, l);
     c0 = h ^ p.b2;
     c1 = l;
     c2 = c3 ^ p.c2;
     // round 3 (c3 of round 2 is uniform and folded into e3)
     {
         uint32_t h0, l0, h1, l1;
-        mulhilo_c<PHILOX_M0, SPLIT>(c0, h0, l0);
-        mulhilo_c<PHILOX_M1, SPLIT>(c2, h1, l1);
+        mulhilo_c<PHILOX_M0, (M >> 3) & 1>(c0, h0, l0);
+        mulhilo_c<PHILOX_M1, (M >> 3) & 1>(c2, h1, l1);
         c0 = h1 ^ c1 ^ p.k0_3;
         c1 = l1;
         c2 = h0 ^ p.e3;
         c3 = l0;
     }
-#pragma unroll
-    for (int r = 0; r < 6; r++) philox_round_d<SPLIT>(c0, c1, c2, c3, p.rk0[r], p.rk1[r]);
+    philox_round_d<(M >> 4) & 1>(c0, c1, c2, c3, p.rk0[0], p.rk1[0]);
+    philox_round_d<(M >> 5) & 1>(c0, c1, c2, c3, p.rk0[1], p.rk1[1]);
+    philox_round_d<(M >> 6) & 1>(c0, c1, c2, c3, p.rk0[2], p.rk1[2]);
+    philox_round_d<(M >> 7) & 1>(c0, c1, c2, c3, p.rk0[3], p.rk1[3]);
+    philox_round_d<(M >> 8) & 1>(c0, c1, c2, c3, p.rk0[4], p.rk1[4]);
+    philox_round_d<(M >> 9) & 1>(c0, c1, c2, c3, p.rk0[5], p.rk1[5]);
     return make_uint4(c0, c1, c2, c3);
 }
 

@@ -396,9 +396,17 @@ static int launch_fill_v(const FillArgs<ALG> &a, cudaStream_t st) {
     } else if constexpr (OUT == OUT_NORMAL) {
         if constexpr (TUNING && ALG == PHILOX && !SKIP) {
             // CBRNG_BM_SPLIT=1: Philox mulhilo as IMAD.HI + IMAD (V 1), measured 10 % slower (profiles/r2d_tune.md)
-            static const int split = tuning_knob("CBRNG_BM_SPLIT", 0, 0, 1);
+            // 2..5: only some rounds split (round bit masks 0x2AA, 0x154, 0x3F0, 0x00E)
+            static const int split = tuning_knob("CBRNG_BM_SPLIT", 0, 0, 5);
             static const int lay = tuning_knob("CBRNG_BM_LAYOUT", BM_LAYOUT_DEFAULT, 0, 12);
-            return split ? launch_normal_layout<ALG, SKIP, 1>(a, st, lay) : launch_normal_layout<ALG, SKIP, V>(a, st, lay);
+            switch (split) {
+                case 1: return launch_normal_layout<ALG, SKIP, 1>(a, st, lay);
+                case 2: return launch_normal<ALG, SKIP, 0x2AA, BM_ILP, BM_LC, BM_SC, BM_NT, BM_MB>(a, st);
+                case 3: return launch_normal<ALG, SKIP, 0x154, BM_ILP, BM_LC, BM_SC, BM_NT, BM_MB>(a, st);
+                case 4: return launch_normal<ALG, SKIP, 0x3F0, BM_ILP, BM_LC, BM_SC, BM_NT, BM_MB>(a, st);
+                case 5: return launch_normal<ALG, SKIP, 0x00E, BM_ILP, BM_LC, BM_SC, BM_NT, BM_MB>(a, st);
+                default: return launch_normal_layout<ALG, SKIP, V>(a, st, lay);
+            }
         } else if constexpr (ALG != PHILOX) {
             return launch_normal<ALG, SKIP, V, 4, 8, 2, 512, 0>(a, st);  // wider cipher state
         } else {

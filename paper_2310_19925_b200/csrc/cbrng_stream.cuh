@@ -13,7 +13,7 @@ template <> struct StreamOf<SQUARES> { using T = SquaresStream; };
 
 
 // V selects a code variant per algorithm. Philox: V = 1 splits each mulhilo
-// into IMAD.HI + IMAD (philox_stream_block). Threefry (adds "forced" = emitted as
+// into IMAD.HI + IMAD, V > 1 the rounds of the bit mask V (philox_stream_block). Threefry (adds "forced" = emitted as
 // IMAD on the FMA-heavy pipe instead of IADD3 on the ALU pipe; "mul" rotations
 // = IMAD.WIDE by 2^r instead of SHF.L.W):
 //   V = 0 compiler-scheduled;             V = 1: forced round adds + 10 mul rotations;
@@ -21,7 +21,7 @@ template <> struct StreamOf<SQUARES> { using T = SquaresStream; };
 //   V = 4: forced round + injection adds; V = 5/6/7/8: V4 + 2/4/6/8 mul rotations.
 template <int ALG, int V>
 __device__ __forceinline__ uint4 block_at(const typename StreamOf<ALG>::T &p, uint32_t bc) {
-    if constexpr (ALG == PHILOX) return philox_stream_block<V == 1>(p, bc);  // V 1: split mulhilo
+    if constexpr (ALG == PHILOX) return philox_stream_block<V>(p, bc);  // V: split-mulhilo round mask (1 = all)
     else if constexpr (V == 0) return threefry_stream_block<0, false>(p, bc);
     else if constexpr (V == 1) return threefry_stream_block<10, true>(p, bc);
     else if constexpr (V == 2) return threefry_stream_block<0, true>(p, bc);

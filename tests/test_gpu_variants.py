@@ -176,7 +176,7 @@ print(json.dumps(bad))
 @pytest.mark.parametrize("env", [
     {"CBRNG_BROWNIAN_TAB": "0"}, {"CBRNG_BROWNIAN_TAB": "2"}, {"CBRNG_BROWNIAN_PINGPONG": "0"}, {"CBRNG_BROWNIAN_PDL": "0"},
     {"CBRNG_GRID_MULT": "0"}, {"CBRNG_GRID_MULT": "16"}, {"CBRNG_TY_GRID": "8"}, {"CBRNG_BM_GRID": "4"},
-    *({"CBRNG_BM_LAYOUT": str(k)} for k in range(13)), {"CBRNG_BM_SPLIT": "1"},
+    *({"CBRNG_BM_LAYOUT": str(k)} for k in range(13)), *({"CBRNG_BM_SPLIT": str(k)} for k in range(1, 6)),
     {"CBRNG_BROWNIAN_SPLIT": "1"}, {"CBRNG_BROWNIAN_SPLIT": "2"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_misc_knobs(env):
