@@ -21,7 +21,8 @@ pytestmark = pytest.mark.gpu
 
 M32, M64 = 0xFFFFFFFF, 0xFFFFFFFFFFFFFFFF
 ALGS = ["philox", "threefry", "squares"]
-SETTINGS = settings(max_examples=60, deadline=None, suppress_health_check=[HealthCheck.function_scoped_fixture])
+SETTINGS = settings(max_examples=60, deadline=None, derandomize=True,
+                    suppress_health_check=[HealthCheck.function_scoped_fixture])
 
 
 @pytest.fixture(scope="module")
