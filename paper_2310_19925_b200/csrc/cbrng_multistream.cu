@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 
 #include "cbrng_internal.cuh"
+#include "cbrng_stream.cuh"
 
 namespace cbrng {
 
@@ -458,8 +459,68 @@ static int launch_staged(const PrefixArgs &a, cudaStream_t st) {
     return launch_staged_cv<ALG, OUT, C0>(a, st);
 }
 
+// Rows of 256 words of a block cipher (configs[4]) with LPR lanes per row and
+// no staging: the LPR lanes of a row each set up the row's stream (the folded
+// key material of philox/threefry_stream_setup, LPR-fold redundant) and take
+// blocks sub, sub + LPR, ... (64 / LPR blocks in flight per lane), so each
+// store instruction writes 32 / LPR rows x LPR consecutive 16-byte blocks
+// (64-byte row segments at LPR = 4, full 128-byte lines at 8) straight from
+// registers. Against the one-thread-per-row staged kernel (B200, 2^22 x 256,
+// profiles/r2k_tune.md): Philox u32 6174 -> 7120 GB/s at LPR 4, f32 6084 ->
+// 6424; Threefry u32 3510 -> 3652 and f32 3202 -> 3357 at LPR 8.
+template <int ALG, int OUT, int CV, int LPR, int MB>
+__global__ void __launch_bounds__(256, MB) rowsplit_kernel(const __grid_constant__ PrefixArgs a) {
+    static_assert(ALG == PHILOX || ALG == THREEFRY, "block ciphers only");
+    constexpr uint32_t NB = 64, RPW = 32 / LPR, ILP = NB / LPR;
+    const uint32_t lane = threadIdx.x & 31, sub = lane % LPR, rw = lane / LPR;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r0 = warp * RPW; r0 < a.n_streams; r0 += nwarps * RPW) {
+        const uint64_t r = r0 + rw;
+        if (r >= a.n_streams) continue;
+        uint4 w[ILP];
+        if constexpr (ALG == PHILOX) {
+            const PhiloxStream p = philox_stream_setup(seed_of(a, r), ctr_of(a, r));
+#pragma unroll
+            for (uint32_t j = 0; j < ILP; j++) w[j] = philox_stream_block(p, sub + LPR * j);
+        } else {
+            ThreefryStream p = threefry_stream_setup(seed_of(a, r), ctr_of(a, r));
+            p.one = c_one;  // keep the forced adds on the FMA-heavy pipe (RowGen<THREEFRY>)
+#pragma unroll
+            for (uint32_t j = 0; j < ILP; j++) w[j] = threefry_stream_block<0, true, true>(p, sub + LPR * j);
+        }
+        const uint64_t row = CBRNG_CEILING ? (r & 2047u) : r;  // ceiling build: one L2-resident ring
+#pragma unroll
+        for (uint32_t j = 0; j < ILP; j++) store4<OUT, CV>(a.out, row * 256 + 4ull * (sub + LPR * j), w[j], a.m24);
+    }
+}
+
+template <int ALG, int OUT, int LPR>
+static int launch_rowsplit(const PrefixArgs &a, cudaStream_t st) {
+    constexpr int CV = ms_cv_default<ALG>();
+    auto k = rowsplit_kernel<ALG, OUT, CV, LPR, 0>;
+    const uint64_t work = (a.n_streams + 8 * (32 / LPR) - 1) / (8 * (32 / LPR));
+    k<<<grid_for(k, 256, 0, work ? work : 1), 256, 0, st>>>(a);
+    return check_launch("rowsplit_kernel");
+}
+
+// Lanes per 256-word row of the block ciphers (0: the staged kernel).
+template <int ALG> constexpr int ms_split_default() { return ALG == PHILOX ? 4 : ALG == THREEFRY ? 8 : 0; }
+
 template <int ALG, int OUT>
 static int launch_prefix(const PrefixArgs &a, cudaStream_t st) {
+    if constexpr (ALG == PHILOX || ALG == THREEFRY) {
+        if (a.nwords == 256 && a.n_streams > 0) {
+            if constexpr (TUNING) {  // CBRNG_MS_SPLIT = 0 (staged) / 4 / 8 / 16
+                static const int lpr = tuning_knob("CBRNG_MS_SPLIT", ms_split_default<ALG>(), 0, 16);
+                if (lpr == 4) return launch_rowsplit<ALG, OUT, 4>(a, st);
+                if (lpr == 8) return launch_rowsplit<ALG, OUT, 8>(a, st);
+                if (lpr == 16) return launch_rowsplit<ALG, OUT, 16>(a, st);
+            } else {
+                return launch_rowsplit<ALG, OUT, ms_split_default<ALG>()>(a, st);
+            }
+        }
+    }
     // Rows of >= 16 words: one thread per stream with the stream setup folded
     // once per row, staged through shared memory (ncu: the warp-per-row kernel
     // spends ~20 % of its FMA-heavy cycles re-deriving the key schedule).

@@ -122,14 +122,17 @@ print(json.dumps(bad))
 """
 
 
-@pytest.mark.parametrize("tma", [0, 1])
-def test_rows256_copy_out(tma):
-    """256-word rows through the LDS/STG copy-out and the TMA-store copy-out."""
+@pytest.mark.parametrize("env", [{"CBRNG_MS_SPLIT": "0", "CBRNG_MS_TMA": "0"}, {"CBRNG_MS_SPLIT": "0", "CBRNG_MS_TMA": "1"},
+                                 {"CBRNG_MS_SPLIT": "4"}, {"CBRNG_MS_SPLIT": "8"}, {"CBRNG_MS_SPLIT": "16"}],
+                         ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_rows256_copy_out(env):
+    """256-word rows through the staged kernel (LDS/STG or TMA-store copy-out) and the
+    lanes-per-row kernel without staging (Philox / Threefry, 4 / 8 / 16 lanes per row)."""
     import torch
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    env = dict(os.environ, CBRNG_MS_TMA=str(tma))
+    env = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-c", CHILD_ROWS256 % str(ROOT)], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]

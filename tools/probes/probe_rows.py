@@ -1,6 +1,6 @@
 """Multi-stream rows of 256 words (2^22 streams), u32 and f32, GB/s, for one generator.
 
-    python tools/probes/probe_rows.py threefry
+    python tools/probes/probe_rows.py threefry [--tuning]   (--tuning: the CBRNG_* knobs' build)
 """
 import sys
 from pathlib import Path
@@ -10,6 +10,9 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from paper_2310_19925_b200 import _lib  # noqa: E402
 
+if "--tuning" in sys.argv:
+    _lib.use_tuning_build()
+    sys.argv.remove("--tuning")
 alg = ("philox", "threefry", "squares", "tyche").index(sys.argv[1] if len(sys.argv) > 1 else "threefry")
 L = _lib.lib()
 s = int(torch.cuda.current_stream().cuda_stream)

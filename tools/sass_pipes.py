@@ -170,8 +170,16 @@ def fill_work(so: str, alg: int, out: int) -> dict:
 
 
 def rows_work(so: str, alg: int, out: int) -> dict:
-    """Per word of 256-word rows (staged_prefix_kernel<..., 256>): the group loop
-    (16 words per thread) plus, for Tyche, the per-row warm-up over 256 words."""
+    """Per word of 256-word rows. Philox / Threefry: rowsplit_kernel<ALG, OUT, CV, LPR, MB>,
+    whose row loop holds the row's stream setup and its 64 / LPR blocks per lane. The
+    others: staged_prefix_kernel<..., 256>, the group loop (16 words per thread) plus,
+    for Tyche, the per-row warm-up over 256 words."""
+    if alg in (0, 1):
+        name, ins = find(so, rf"rowsplit_kernel<{alg}, {out}, \d+, \d+, 0>")
+        lpr = int(re.search(rf"rowsplit_kernel<{alg}, {out}, \d+, (\d+),", name).group(1))
+        lo, hi = hot_loop(ins, must="STG")
+        w = pipes(mix(ins, lo, hi), 4 * (64 // lpr))
+        return {"kernel": name, "unit": "word", "loop": [hex(lo), hex(hi)], **{k: round(v, 3) for k, v in w.items()}}
     name, ins = find(so, rf"staged_prefix_kernel<{alg}, {out}, true, \d+, 4, 256>")
     # the kernel has two group loops: the generic one (per-row store predicates: an
     # ISETP per row slot) and the full-warp 256-word-row path that every launch of
