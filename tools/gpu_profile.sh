@@ -5,7 +5,7 @@ TAG=${PROFILE_TAG:-rX}
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --quick --steps 2 --warmup 1 > gpurun_out/ncu_launch_bench.log 2>&1
 timeout 1200 ncu --set full --clock-control none --import-source on \
-    -k regex:"fill_kernel|normal_fill|staged_prefix|brownian_fused|brownian_steps" -c ${NCU_COUNT:-8} \
+    -k regex:"fill_kernel|normal_fill|staged_prefix|rowsplit|brownian_fused|brownian_steps" -c ${NCU_COUNT:-8} \
     -o /tmp/prof_full python tools/prof_kernels.py ${NCU_WHICH:-fill tyche prefix normal brownian} > gpurun_out/ncu_full.log 2>&1
 python tools/summarize_profiles.py "$TAG" gpurun_out/launches.csv /tmp/prof_full.ncu-rep > gpurun_out/summarize.log 2>&1
 mkdir -p gpurun_out/profiles
