@@ -116,3 +116,24 @@ def test_generator_windows_match_reference_order(cb, oracle):
         g = cb.make_generator(alg, 5, 6)
         got = [g.next_u32() for _ in range(64 + 128 + 256 + 3)]
         assert np.array_equal(np.array(got, np.uint32), oracle.stream_words(alg, 5, 6, len(got))), alg
+
+
+def test_scalar_calls_from_threads(cb, oracle):
+    """cbrng_scalar is reentrant: 8 host threads interleaving block functions and
+    generator windows (the reference drives its nogil kernels from a thread pool,
+    brownian.py:185-191) get the same results as serial calls."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def work(t):
+        bad = 0
+        for i in range(100):
+            key, ctr = (t, i), (i, t, 7, 9)
+            bad += tuple(cb.philox_block(key, ctr)) != tuple(oracle.philox_block(key, ctr))
+            bad += cb.squares_round(cb.squares_key(t), i) != oracle.squares_round(oracle.squares_key(t), i)
+        g = cb.make_generator(("philox", "threefry", "squares", "tyche")[t % 4], t, 3)
+        got = np.array([g.next_u32() for _ in range(300)], np.uint32)
+        bad += not np.array_equal(got, oracle.stream_words(g.algorithm.name.lower(), t, 3, 300))
+        return bad
+
+    with ThreadPoolExecutor(8) as ex:
+        assert sum(ex.map(work, range(8))) == 0
